@@ -1,0 +1,95 @@
+/*
+ * synth.c -- seeded synthetic input generators shared by the oracle tests and
+ * the product tests / bench.  Holds NONE of the method's arithmetic (no rANS,
+ * no model quantisation, no metadata): it only turns counter-based SplitMix64
+ * draws into bytes through integer inverse-CDF threshold tables that the
+ * Python side (synth/__init__.py) computes from the workload recipes in
+ * DESIGN.md "Input recipe".
+ *
+ * Draw i of a stream with seed s is  u_i = mix64(s + (i + 1) * GAMMA)
+ * (the SplitMix64 output at position i), so any sub-range can be generated
+ * independently and the result does not depend on the thread count.
+ * Byte_i = #{k : thr[k] <= u_i} clamped to 255, where thr[] is the table's
+ * cumulative distribution scaled to 2^64.
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <pthread.h>
+
+#define GAMMA 0x9E3779B97F4A7C15ULL
+
+static inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+static inline uint8_t draw_byte(uint64_t u, const uint64_t *thr) {
+  /* branch-free lower bound over 256 sorted thresholds: count of thr[k] <= u */
+  uint32_t k = 0;
+  for (uint32_t step = 128; step > 0; step >>= 1)
+    if (thr[k + step - 1] <= u) k += step;
+  return (uint8_t)(k > 255 ? 255 : k);
+}
+
+typedef struct {
+  uint8_t *out;
+  uint64_t begin, end; /* absolute draw indices */
+  uint64_t seed;
+  const uint64_t *tables; /* n_tables x 256 */
+  uint32_t n_tables;
+  uint64_t tile; /* symbols per tile (table chosen per tile); 0 = single table */
+} job_t;
+
+static void *run_job(void *arg) {
+  job_t *j = (job_t *)arg;
+  const uint64_t *thr = j->tables;
+  uint64_t cur_tile = UINT64_MAX;
+  for (uint64_t i = j->begin; i < j->end; ++i) {
+    if (j->tile) {
+      uint64_t t = i / j->tile;
+      if (t != cur_tile) {
+        cur_tile = t;
+        uint64_t h = mix64((j->seed ^ 0xD1B54A32D192ED03ULL) + (t + 1) * GAMMA);
+        thr = j->tables + 256 * (h % j->n_tables);
+      }
+    }
+    uint64_t u = mix64(j->seed + (i + 1) * GAMMA);
+    j->out[i - j->begin] = draw_byte(u, thr);
+  }
+  return NULL;
+}
+
+/* Fill out[0..count) with draws [start, start+count) of stream `seed`.
+ * tables: n_tables x 256 thresholds (uint64, non-decreasing per table).
+ * tile == 0: table 0 for every draw; else draw i uses the table picked by a
+ * hash of (seed, i / tile).  threads <= 0 means 1. Returns 0. */
+int synth_fill(uint8_t *out, uint64_t start, uint64_t count, uint64_t seed,
+               const uint64_t *tables, uint32_t n_tables, uint64_t tile,
+               int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  if (count < (1u << 20)) threads = 1;
+  pthread_t th[64];
+  job_t jobs[64];
+  for (int t = 0; t < threads; ++t) {
+    uint64_t b = count * (uint64_t)t / (uint64_t)threads;
+    uint64_t e = count * (uint64_t)(t + 1) / (uint64_t)threads;
+    jobs[t].out = out + b;
+    jobs[t].begin = start + b;
+    jobs[t].end = start + e;
+    jobs[t].seed = seed;
+    jobs[t].tables = tables;
+    jobs[t].n_tables = n_tables ? n_tables : 1;
+    jobs[t].tile = tile;
+  }
+  for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, run_job, &jobs[t]);
+  run_job(&jobs[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}
+
+/* Raw SplitMix64 draws (for tests that need random words / fuzz parameters). */
+void synth_u64(uint64_t *out, uint64_t start, uint64_t count, uint64_t seed) {
+  for (uint64_t i = 0; i < count; ++i) out[i] = mix64(seed + (start + i + 1) * GAMMA);
+}
