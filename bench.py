@@ -1,0 +1,421 @@
+#!/usr/bin/env python3
+"""Benchmark: Recoil parallel rANS decode on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config config2] [--impl reference]
+
+A *step* is one pass of the whole hot path over one synthetic
+stream: the sm_100a decode kernel over every split task of this rank's shard
+(task table, LUT and word slice already resident in HBM; row a1, the
+host-side task-table expansion, is part of the e2e leg).  ``value`` is the
+whole-job decoded GB/s = symbols decoded by all ranks per step x K / max over
+ranks of the device time of the K steps (CUDA events on the decode stream,
+L2 flushed with a 256 MiB write before every step, outside the events).
+
+Multi-GPU (torchrun, one process per GPU): one stream of N x the config's
+size is sharded by contiguous split ranges (recoil_shard_plan), each rank
+decodes its own shard; no collective on the data path -> "scaling": "weak".
+
+``--impl reference`` times the oracle (plain C, single thread) -- this tier's
+reference arm -- on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "decoded GB/s per GPU and 8×B200 box; compressed-size overhead vs split count"
+
+CONFIGS = {
+    # name: (kind, symbols, lambda, description)  -- BASELINE.json "configs"
+    "config1": ("exp", 1 << 20, 50.0, "1 MiB exponential (lambda=50) bytes, n=11, 16 splits"),
+    "config2": ("text", 100 << 20, 0.0, "100 MiB text-like (Zipf-96, ~5.09 bit/B) bytes, n=11, "
+                                         "splits tuned to the kernel's resident warps"),
+    "config3": ("exp", 1 << 30, 50.0, "1 GiB exponential (lambda=50) bytes, n=11, occupancy-tuned splits"),
+    "config5": ("image", 1 << 30, 0.0, "image-residual-like bytes (Laplace mixture, ~2.3 bit/B), n=11, "
+                                       "sharded by split range (1 GiB per GPU)"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report that instead of clocks
+            self.err = str(e)
+        self.period = period_s
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(self.period)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join()
+        self.sample()
+
+    def report(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable: " + self.err}
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_stream(cfg: str, world: int, prob_bits: int = 11):
+    import synth
+    kind, n, lam, _ = CONFIGS[cfg]
+    n_total = n * world
+    sym = synth.workload(kind, n_total, seed=synth.seed_for(int(cfg[-1]), lam), lam=lam or 50.0)
+    return sym
+
+
+def cpu_oracle_decode_rate(container: np.ndarray, sample_tasks: int | None, reps: int = 1):
+    """Time the oracle (plain C, single thread) decoding `sample_tasks` evenly spaced tasks
+    (None = every task).  Returns (GB/s, symbols per rep, seconds per rep, description)."""
+    import oracle
+    c = container.tobytes()
+    info = oracle.container_info(c)
+    M, N = info["M"], info["N"]
+    out = np.zeros(max(N, 1), dtype=np.uint8)
+    if sample_tasks is None or sample_tasks >= M:
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = oracle.recoil_decode(c)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return N / best / 1e9, N, best, f"oracle or_recoil_decode of all {M} tasks ({N} symbols), best of {reps}"
+    tasks = np.unique(np.linspace(0, M - 1, sample_tasks).astype(int))
+    best = None
+    for _ in range(reps):
+        nsym = 0
+        t0 = time.perf_counter()
+        for t in tasks:
+            _, lo, hi = oracle.recoil_decode_task(c, int(t), out)
+            nsym += hi - lo + 1
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return nsym / best / 1e9, nsym, best, f"oracle or_recoil_decode_task on {len(tasks)} of {M} tasks ({nsym} symbols)"
+
+
+def run_reference(args, rank, world):
+    """Reference arm of this tier: the oracle as it stands, on the host cores."""
+    if rank != 0:
+        return 0
+    import oracle  # noqa: F401
+    from paper_2306_12141_b200 import recoil as R
+    sym = make_stream(args.config, world)
+    f = R.recoil_build_model(np.bincount(sym, minlength=256).astype(np.uint64), 11)
+    M = args.splits or 11840 * world
+    c = R.recoil_encode(sym, f, 11, M)
+    M = R.recoil_inspect(c)["n_splits"]
+    per_step = max(1, M // 64)  # ~1/64 of the stream per step: bounded sample
+    times, nsyms = [], []
+    for i in range(args.warmup + args.steps):
+        gbs, nsym, dt, desc = cpu_oracle_decode_rate(c, per_step)
+        if i >= args.warmup:
+            times.append(dt)
+            nsyms.append(nsym)
+    total_t, total_n = sum(times), sum(nsyms)
+    value = total_n / total_t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total_t / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.config + ": " + CONFIGS[args.config][3], "n_symbols": int(len(sym)),
+                   "splits": M, "prob_bits": 11, "lanes": 32},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{per_step} evenly spaced split tasks per step ({desc.split('(')[-1][:-1]})"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
+    ap.add_argument("--waves", type=int, default=2, help="splits per GPU = waves x resident warps")
+    ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip partitioned / size-overhead legs")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    from paper_2306_12141_b200 import recoil as R
+    import __graft_entry__
+    if rank == 0 or not os.path.exists(R.LIB_PATH):
+        __graft_entry__.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+        dist.barrier()
+    R.load()
+
+    # ---------------- setup (untimed): synthetic stream, encode, shard plan ----------------
+    t_setup = time.perf_counter()
+    sym = make_stream(args.config, world)
+    N_total = len(sym)
+    hist = np.bincount(sym, minlength=256).astype(np.uint64)
+    f = R.recoil_build_model(hist, 11)
+    warps, sms = R.recoil_decode_occupancy(local, 11)
+    M_gpu = args.splits or (16 if args.config == "config1" else warps * sms * args.waves)
+    c = R.recoil_encode(sym, f, 11, M_gpu * world)
+    info = R.recoil_inspect(c)
+    M = info["n_splits"]
+    bounds = R.recoil_shard_plan(c, world)
+    a, b = bounds[rank], bounds[rank + 1]
+    pinned = torch.empty(len(c), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = c
+    cont = pinned.numpy()
+    stream = torch.cuda.Stream(dev)
+    dec = R.GpuDecoder(cont, local, a, b, stream=stream)
+    plan = dec.plan
+    dec.upload()
+    torch.cuda.synchronize(dev)
+    setup_s = time.perf_counter() - t_setup
+    n_rank = plan["out_hi"] - plan["out_lo"]
+    words_rank = plan["word_count"]
+    alg_bytes = n_rank + 2 * min(words_rank, max(0, info["n_words"] - plan["word_lo"])) + plan["workspace_bytes"]
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # correctness of this rank's span before timing (bit-exact vs the input = the decode's definition)
+    dec.decode()
+    rc, bad = dec.status()
+    got = dec.output().cpu().numpy()
+    ok = rc == 0 and bool((got == sym[plan["out_lo"]:plan["out_hi"]]).all())
+    if not ok:
+        log(f"rank {rank}: decode mismatch rc={rc} bad={bad}")
+
+    def timed_decode(decoder, steps, warmup):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for _ in range(warmup):
+            flush_buf.fill_(1)
+            decoder.decode()
+        torch.cuda.synchronize(dev)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            for i in range(steps):
+                flush_buf.fill_(2)      # evict L2 (256 MiB > 126 MB) outside the events
+                ev[i][0].record(stream)
+                decoder.decode()
+                ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+        return [s.elapsed_time(e) for s, e in ev]
+
+    clocks = ClockSampler(local)
+    with clocks:
+        times = timed_decode(dec, args.steps, args.warmup)
+    total_ms = float(sum(times))
+    if pg:
+        t = torch.tensor([total_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms = float(t.item())
+        okt = torch.tensor([1 if ok else 0], device=dev)
+        pg.all_reduce(okt, op=pg.ReduceOp.MIN)
+        ok = bool(okt.item())
+    value = N_total * args.steps / (total_ms / 1e3) / 1e9
+    my_avg_ms = float(np.mean(times))
+    achieved = alg_bytes / (my_avg_ms / 1e3) / 1e9
+
+    # ---------------- e2e: host container -> host symbols through the C ABI ----------------
+    out_host = torch.empty(max(plan["out_count"], 16), dtype=torch.uint8, pin_memory=True)
+    e2e_times = []
+    ws, words, out_dev = dec.workspace, dec.words, dec.out
+    steps_e2e = max(3, min(args.steps, 20))
+    for i in range(args.warmup + steps_e2e):
+        torch.cuda.synchronize(dev)
+        if pg:
+            pg.barrier()
+        t0 = time.perf_counter()
+        h = R.recoil_decoder_create(cont, a, b)                       # a1 on the host
+        R.recoil_decoder_upload(h, ws.data_ptr(), words.data_ptr(), stream.cuda_stream)   # H2D
+        R.recoil_decode(h, ws.data_ptr(), words.data_ptr(), out_dev.data_ptr(), stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            out_host[:plan["out_count"]].copy_(out_dev[:plan["out_count"]], non_blocking=True)  # D2H
+        rc_e2e, _ = R.recoil_decoder_status(h, ws.data_ptr(), stream.cuda_stream)  # syncs the stream
+        dt = time.perf_counter() - t0
+        R.recoil_decoder_destroy(h)
+        if rc_e2e != 0:
+            ok = False
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = float(np.mean(e2e_times))
+    if pg:
+        t = torch.tensor([e2e_s], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = N_total / e2e_s / 1e9
+    ok = ok and bool((out_host.numpy()[plan["out_lo"] - plan["out_base"]:plan["out_hi"] - plan["out_base"]] ==
+                      sym[plan["out_lo"]:plan["out_hi"]]).all())
+
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        # the paper's comparison: conventional partitioned decoder at the same count
+        pc = R.recoil_partitioned_encode(sym, f, 11, M)
+        pbounds = R.recoil_shard_plan(pc, world)
+        pdec = R.GpuDecoder(pc, local, pbounds[0], pbounds[1], stream=stream)
+        pdec.upload()
+        pt = timed_decode(pdec, args.steps, args.warmup) if world == 1 else None
+        pn = pdec.plan["out_hi"] - pdec.plan["out_lo"]
+        pdec.decode()
+        pok = pdec.status()[0] == 0 and bool((pdec.output().cpu().numpy() ==
+                                              sym[pdec.plan["out_lo"]:pdec.plan["out_hi"]]).all())
+        if pt:
+            extra["partitioned_baseline"] = {
+                "value": round(pn * args.steps / (sum(pt) / 1e3) / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(float(np.mean(pt)), 4), "partitions": M, "bit_exact": pok,
+                "container_bytes": int(len(pc))}
+        c1 = R.recoil_encode(sym, f, 11, 1)
+        p1 = R.recoil_partitioned_encode(sym, f, 11, 1)
+        small = R.recoil_combine_splits(c, 16)
+        extra["size_overhead"] = {
+            "baseline_bytes_M1": int(len(c1)),
+            "recoil": {"splits": M, "bytes": int(len(c)), "overhead_bytes": int(len(c) - len(c1)),
+                       "bytes_per_split": round((len(c) - len(c1)) / max(1, M - 1), 2)},
+            "partitioned": {"partitions": M, "bytes": int(len(pc)), "overhead_bytes": int(len(pc) - len(p1)),
+                            "bytes_per_partition": round((len(pc) - len(p1)) / max(1, M - 1), 2)},
+            "recoil_combined_to_16": {"bytes": int(len(small)), "overhead_bytes": int(len(small) - len(c1))},
+        }
+        pdec.close()
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        gbs, nsym, dt, desc = cpu_oracle_decode_rate(c, None if N_total <= (256 << 20) else 256, reps=1)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": desc, "seconds": round(dt, 3)}
+        t0 = time.perf_counter()
+        threads = os.cpu_count() or 1
+        out_cpu = R.recoil_decode_cpu(cont, threads)
+        dt_mt = time.perf_counter() - t0
+        extra["cpu_mt_library"] = {"value": round(N_total / dt_mt / 1e9, 4), "unit": "GB/s", "threads": threads,
+                                   "bit_exact": bool((out_cpu == sym).all()),
+                                   "note": "recoil_decode_cpu: scalar MT host decoder (baseline, not a fallback)"}
+
+    prof = {}
+    pf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(pf):
+        try:
+            prof = json.load(open(pf)).get(f"{args.config}:{M_gpu}", {})
+        except Exception:
+            prof = {}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    traffic = prof.get("dram_bytes_per_launch")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config + ": " + CONFIGS[args.config][3], "n_symbols": int(N_total),
+                       "n_symbols_per_gpu": int(CONFIGS[args.config][1]), "splits": int(M),
+                       "splits_rule": f"{args.waves} waves x {warps} resident warps/SM x {sms} SMs per GPU"
+                       if not args.splits and args.config != "config1" else "fixed",
+                       "compressed_bytes": int(len(c)), "prob_bits": 11, "lanes": 32,
+                       "parallelism": f"split-range shards x{world}",
+                       "l2": "flushed before every timed step (256 MiB write, outside the events)"},
+            "bit_exact": ok,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "recoil_decode_kernel<11>",
+                         "algorithmic_bytes_per_launch": int(alg_bytes),
+                         "note": "achieved = (decoded bytes written + compressed words read + task table) / "
+                                 "event-timed decode; peak = MEASURED_PEAKS.json hbm_gbs (burst)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(plan["upload_bytes"]), "d2h_bytes_per_step": int(plan["out_count"]),
+                    "note": "per step: host parse + task expansion, H2D words+tables from pinned memory, "
+                            "kernel, D2H of the symbols, status read"},
+            "gpu_launches": int(args.steps * dec.launches()),
+            "clocks": clocks.report(),
+            "setup_s": round(setup_s, 2),
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    dec.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,203 @@
+/*
+ * recoil.h -- C ABI of the B200-native Recoil library (librecoil.so).
+ *
+ * Recoil (Lin et al., arXiv 2306.12141; /root/reference/PAPER.md cited as
+ * P:<line>) makes ONE W = 32-way interleaved rANS bitstream decodable from
+ * the middle by storing, at chosen renormalisation points ("splits"), each
+ * lane's 16-bit state and symbol group and the bitstream offset; decoding of
+ * the splits then runs in parallel, one warp per split, on sm_100a.
+ *
+ * Fixed parameters (tab:rans_params P:400-423): 32-bit states, L = 2^16,
+ * b = 16-bit words, 8-bit symbols, W = 32 lanes, 1 <= n <= 16 probability
+ * bits for encoding; the GPU decoder supports n <= 12 (packed LUT).
+ * Symbol i (0-based) belongs to lane i mod 32 and group i / 32.
+ *
+ * Conventions for every call:
+ *  - Return value: RECOIL_OK (0) or a negative RECOIL_E_* code; no call
+ *    aborts the process.  recoil_strerror() names a code.
+ *  - The caller owns every buffer passed in, host or device; the library
+ *    never frees or retains them past the call, except as stated for
+ *    recoil_decoder_upload (host source must stay valid until the stream
+ *    passes the copy).  Handles own only host memory.
+ *  - Device memory and streams come from the caller (PyTorch in this repo);
+ *    `cuda_stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Sizes: passing out == NULL stores the required (for encode: an upper
+ *    bound) length in *len and returns RECOIL_OK; a too-small buffer returns
+ *    RECOIL_E_BUFFER with the required length in *len.
+ *  - Reentrant; no global state.  A handle is used by one thread at a time.
+ *  - Containers are little-endian byte strings; see DESIGN.md "Container".
+ */
+#ifndef RECOIL_H
+#define RECOIL_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RECOIL_OK 0
+#define RECOIL_E_ARG (-1)          /* bad argument (NULL pointer, range)          */
+#define RECOIL_E_EMPTY (-2)        /* model from an empty histogram        */
+#define RECOIL_E_ALPHABET (-3)     /* more distinct symbols than 2^n       */
+#define RECOIL_E_ZERO_FREQ (-4)    /* symbol to encode has f = 0          */
+#define RECOIL_E_OVERFLOW (-5)     /* a metadata value does not fit its field     */
+#define RECOIL_E_BAD_MAGIC (-6)    /* not a Recoil / partitioned container        */
+#define RECOIL_E_VERSION (-7)      /* unsupported version / symbol width          */
+#define RECOIL_E_TRUNCATED (-8)    /* container shorter than its header says      */
+#define RECOIL_E_INCONSISTENT (-9) /* metadata inconsistent               */
+#define RECOIL_E_UNDERFLOW (-10)   /* device: a task read below its word slice    */
+#define RECOIL_E_SYNC (-11)        /* device: end state != (x = L, cursor = -1)   */
+#define RECOIL_E_CUDA (-12)        /* a CUDA runtime call failed                  */
+#define RECOIL_E_NOMEM (-13)       /* host allocation failed                      */
+#define RECOIL_E_BUFFER (-14)      /* output buffer too small (*len = required)   */
+#define RECOIL_E_UNSUPPORTED (-15) /* valid but outside the GPU path (n > 12)     */
+
+const char *recoil_strerror(int status);
+
+/* ---------------------------------------------------------------------- */
+/* Model                                                                   */
+/* ---------------------------------------------------------------------- */
+
+/* Quantised PDF f(t) with sum f = 2^prob_bits.  The paper does not
+ * give its quantiser: floor(h 2^n / total), present symbols raised to
+ * 1, shortfall by largest remainder (ties: smaller symbol), excess (from the
+ * raise) taken from the largest f (ties: smaller count, then smaller symbol).
+ * hist: 256 counts.  freqs_out: 256 entries.  Errors: E_ARG (n outside 1..16),
+ * E_EMPTY, E_ALPHABET. */
+int recoil_build_model(const uint64_t hist[256], uint32_t prob_bits, uint32_t freqs_out[256]);
+
+/* ---------------------------------------------------------------------- */
+/* Encode / combine / inspect (host)                                       */
+/* ---------------------------------------------------------------------- */
+
+/* Serial 32-way interleaved rANS encode (Eq. 1, Eq. 3) of
+ * symbols[0..n_symbols) under freqs (sum = 2^prob_bits), plus the split
+ * heuristic (reading Z10') choosing up to n_splits - 1
+ * split points (the backward scan of P:301 gives each point's anchors), and
+ * the difference-coded metadata.  Result: a Recoil container
+ * ("RCL1") in container[0..*container_len).  Fewer splits than requested are
+ * produced when the stream has too few renormalisation points.
+ * container == NULL: *container_len = an upper bound on the size.
+ * Errors: E_ARG, E_ZERO_FREQ, E_OVERFLOW, E_BUFFER, E_NOMEM. */
+int recoil_encode(const uint8_t *symbols, uint64_t n_symbols, const uint32_t freqs[256],
+                  uint32_t prob_bits, uint32_t n_splits, uint8_t *container,
+                  uint64_t *container_len);
+
+/* Decoder-adaptive combine: keep the split points at
+ * 1-based positions k, 2k, ... with k = ceil(M / target_splits) and rewrite
+ * the metadata for the new M; the word stream is copied verbatim.
+ * target_splits >= M: byte-identical copy.  Errors: E_ARG, container errors,
+ * E_BUFFER. */
+int recoil_combine_splits(const uint8_t *in, uint64_t in_len, uint32_t target_splits, uint8_t *out,
+                          uint64_t *out_len);
+
+typedef struct {
+  uint64_t n_symbols;    /* N */
+  uint64_t n_words;      /* B (16-bit words) */
+  uint32_t n_splits;     /* M (tasks); partitions for a partitioned container */
+  uint32_t prob_bits;    /* n */
+  uint32_t lanes;        /* W (32) */
+  uint32_t partitioned;  /* 0 = Recoil "RCL1", 1 = partitioned "RCV1" */
+  uint64_t header_bytes; /* fixed header + model block */
+  uint64_t meta_bytes;   /* final states + split metadata (or offset table + states) */
+  uint64_t word_bytes;   /* 2 B */
+  uint64_t total_bytes;
+} recoil_info;
+
+/* Parse and validate a container (either kind).  Errors: container errors. */
+int recoil_inspect(const uint8_t *container, uint64_t len, recoil_info *info);
+
+/* Conventional "partitioning symbols" codec for the paper's
+ * comparison: partition p = groups [floor(p G/P), floor((p+1) G/P)), each an
+ * independent 32-way interleaved codec; offset table + final states.
+ * container == NULL: upper bound.  Errors as recoil_encode. */
+int recoil_partitioned_encode(const uint8_t *symbols, uint64_t n_symbols, const uint32_t freqs[256],
+                              uint32_t prob_bits, uint32_t n_partitions, uint8_t *container,
+                              uint64_t *container_len);
+
+/* ---------------------------------------------------------------------- */
+/* GPU decode (sm_100a)                                                    */
+/* ---------------------------------------------------------------------- */
+
+typedef struct recoil_decoder recoil_decoder;
+
+/* Layout of one decode plan.  All device buffers are provided by the caller. */
+typedef struct {
+  uint64_t task_begin, task_end; /* tasks [begin, end) of the container            */
+  uint32_t n_tasks;              /* tasks with work in this plan                    */
+  uint32_t prob_bits;
+  uint64_t word_lo;              /* d_words[0] holds stream word word_lo (mult. of 256) */
+  uint64_t word_count;           /* d_words must hold word_count words (mult. of 256)   */
+  uint64_t out_lo, out_hi;       /* this plan writes symbols [out_lo, out_hi)            */
+  uint64_t out_base;             /* d_out[0] is symbol out_base (out_lo & ~511)          */
+  uint64_t out_count;            /* d_out must hold out_count (>= out_hi - out_base) bytes */
+  uint64_t workspace_bytes;      /* d_workspace size (LUT + task table + status)       */
+  uint64_t upload_bytes;         /* bytes recoil_decoder_upload copies host->device     */
+} recoil_plan;
+
+/* Host half of the path (DESIGN.md row a1): parse the container
+ * and expand the split metadata of tasks [task_begin, task_end) into the
+ * per-warp task table (task_end = UINT64_MAX: all tasks).  Task t < M-1
+ * enters at split point t+1; task M-1 enters from the final
+ * states.  Works on either container kind (partitions = tasks).
+ * The container bytes must stay valid while the handle is used.
+ * Errors: container errors, E_ARG, E_NOMEM, E_UNSUPPORTED (n > 12). */
+int recoil_decoder_create(const uint8_t *container, uint64_t len, uint64_t task_begin,
+                          uint64_t task_end, recoil_decoder **out);
+int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan);
+
+/* Asynchronous host->device copy on cuda_stream of the packed LUT and task
+ * table into d_workspace and of the plan's word slice (zero padded) into
+ * d_words.  Source = the handle's host table and the container bytes.
+ * Errors: E_ARG, E_CUDA. */
+int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uint16_t *d_words, void *cuda_stream);
+
+/* Launch the decode kernel on cuda_stream (asynchronous; stream-ordered):
+ * one warp per split, smem LUT, cp.async word window, ballot/popc
+ * refills, 16-byte output stores.  Writes symbols [out_lo, out_hi) to
+ * d_out[i - out_base]; it may also write, inside d_out[0, out_count), the
+ * neighbouring symbols of partially committed 32-symbol groups (always their
+ * correct decoded values) and padding past N.  Clears and then sets the
+ * device status word.  Errors: E_ARG, E_CUDA. */
+int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint16_t *d_words, uint8_t *d_out,
+                  void *cuda_stream);
+
+/* Synchronise cuda_stream and read the device status word of the last
+ * decode: RECOIL_OK, RECOIL_E_UNDERFLOW or RECOIL_E_SYNC.
+ * *bad_task (may be NULL) = first failing task or UINT64_MAX. */
+int recoil_decoder_status(recoil_decoder *dec, const void *d_workspace, void *cuda_stream,
+                          uint64_t *bad_task);
+
+/* Number of kernel launches one recoil_decode issues (for launch accounting). */
+int recoil_decoder_launches(const recoil_decoder *dec);
+
+void recoil_decoder_destroy(recoil_decoder *dec);
+
+/* Resident warps per SM of the decode kernel on `device` and the SM count
+ * (cudaOccupancyMaxActiveBlocksPerMultiprocessor): the split count
+ * that fills the GPU is warps_per_sm * sm_count * waves. */
+int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU sharding (host planning; each GPU decodes its own task range) */
+/* ---------------------------------------------------------------------- */
+
+/* Split the container's tasks into n_shards contiguous ranges whose
+ * committed symbol counts are as equal as task granularity allows.
+ * task_bounds: n_shards + 1 entries, task_bounds[0] = 0,
+ * task_bounds[n_shards] = M.  Errors: E_ARG, container errors. */
+int recoil_shard_plan(const uint8_t *container, uint64_t len, uint32_t n_shards, uint64_t *task_bounds);
+
+/* ---------------------------------------------------------------------- */
+/* Host baselines (NOT a fallback of the GPU path: separate entry points)  */
+/* ---------------------------------------------------------------------- */
+
+/* Multithreaded CPU Recoil / partitioned decoder: one task per split, up to
+ * `threads` threads (0 = hardware concurrency), scalar code.  out: N bytes.
+ * Errors: container errors, E_UNDERFLOW, E_SYNC. */
+int recoil_decode_cpu(const uint8_t *container, uint64_t len, uint8_t *out, uint32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,212 @@
+// plan.cpp -- row a1 of the hot path: expand the container's
+// split metadata into the per-warp task table, pack the LUT, plan
+// the word slice / output span, and shard task ranges across GPUs (§8(e)).
+//
+// Task t < M-1 enters at split point t+1 (1-based): cursor0 = the point's
+// bitstream offset (the boundary event's word, the first word the task reads),
+// start group = the anchor (max Symbol Group ID), lane j initialised with its
+// 16-bit state in group anchor - diff_j (tab:metadata_codec).  The
+// last task enters from the explicitly transmitted final states; a
+// lane without a symbol in the last group starts one group lower, so the
+// kernel needs no i < N test.  Task t commits [sync_start(point t),
+// sync_start(point t+1) - 1] (reading Z13).
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "../recoil_internal.h"
+
+namespace recoil {
+
+void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint32_t> *lut) {
+  lut->assign((size_t)1 << n, 0);
+  uint32_t F = 0;
+  for (uint32_t s = 0; s < 256; ++s) {
+    for (uint32_t k = 0; k < f[s]; ++k) (*lut)[F + k] = s | (k << 8) | (f[s] << 20);  // s | bias | f
+    F += f[s];
+  }
+}
+
+static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
+
+int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
+                  bool for_gpu) {
+  int rc = parse_container(cbytes, len, &d->c);
+  if (rc) return rc;
+  const Container &c = d->c;
+  if (task_end > c.M) task_end = c.M;
+  if (task_begin > task_end) return RECOIL_E_ARG;
+  if (for_gpu && c.n > kMaxGpuProbBits) return RECOIL_E_UNSUPPORTED;
+  int present = 0;
+  for (int s = 0; s < 256; ++s)
+    if (c.f[s]) {
+      present++;
+      d->single_symbol = s;
+    }
+  if (present != 1) d->single_symbol = -1;
+  if (c.n <= kMaxGpuProbBits) pack_lut(c.f, c.n, &d->lut);
+  d->tasks.clear();
+  d->finals.clear();
+  std::vector<uint64_t> part_start;
+  if (c.partitioned) {
+    part_start.resize(c.M + 1, 0);
+    for (uint32_t p = 0; p < c.M; ++p) part_start[p + 1] = part_start[p] + c.part_words[p];
+  }
+  for (uint64_t t = task_begin; t < task_end; ++t) {
+    TaskRec r;
+    std::memset(&r, 0, sizeof(r));
+    r.task_id = (uint32_t)t;
+    if (!c.partitioned) {
+      int64_t ss, bi;
+      uint64_t lo = 0;
+      if (t > 0) {
+        point_span(c, t - 1, &ss, &bi);
+        lo = (uint64_t)ss;
+      }
+      r.commit_lo = lo;
+      r.end_cursor = lo == 0 ? -1 : kNoEndCheck;
+      if (t + 1 < c.M) {
+        point_span(c, t, &ss, &bi);
+        r.commit_hi = (uint64_t)ss - 1;
+        r.write_hi = kLanes * ((uint64_t)ss / kLanes + 1);  // through the sync completion group
+        r.cursor0 = (int64_t)c.offset[t];
+        r.start_group = (int32_t)c.maxg[t];
+        r.finals_idx = kNoFinals;
+        for (uint32_t j = 0; j < kLanes; ++j)
+          r.lanes[j] = c.state[t * kLanes + j] | ((uint32_t)c.gdiff[t * kLanes + j] << 16);
+      } else {
+        if (c.N == 0) continue;
+        r.commit_hi = c.N - 1;
+        r.write_hi = (c.N + 15) & ~15ull;
+        r.cursor0 = (int64_t)c.B - 1;
+        r.start_group = (int32_t)(c.G - 1);
+        r.finals_idx = (uint32_t)(d->finals.size() / kLanes);
+        d->finals.insert(d->finals.end(), c.finals.begin(), c.finals.end());
+        for (uint32_t j = 0; j < kLanes; ++j) r.lanes[j] = (32 * (c.G - 1) + j < c.N ? 0u : 1u) << 16;
+      }
+    } else {
+      uint64_t gl = t * c.G / c.M, gh = (t + 1) * c.G / c.M;
+      uint64_t lo = kLanes * gl, hi = std::min<uint64_t>(c.N, kLanes * gh);
+      if (lo >= hi) continue;  // empty partition
+      r.commit_lo = lo;
+      r.commit_hi = hi - 1;
+      r.write_hi = (hi + 15) & ~15ull;
+      r.cursor0 = (int64_t)(part_start[t] + c.part_words[t]) - 1;
+      r.end_cursor = (int64_t)part_start[t] - 1;
+      r.start_group = (int32_t)(gh - 1);
+      r.finals_idx = (uint32_t)(d->finals.size() / kLanes);
+      d->finals.insert(d->finals.end(), c.finals.begin() + t * kLanes, c.finals.begin() + (t + 1) * kLanes);
+      for (uint32_t j = 0; j < kLanes; ++j) r.lanes[j] = (kLanes * (gh - 1) + j < hi ? 0u : 1u) << 16;
+    }
+    d->tasks.push_back(r);
+  }
+  // word slice [word_lo, word_hi): chunk aligned, padded
+  recoil_plan &p = d->plan;
+  std::memset(&p, 0, sizeof(p));
+  p.task_begin = task_begin;
+  p.task_end = task_end;
+  p.n_tasks = (uint32_t)d->tasks.size();
+  p.prob_bits = c.n;
+  uint64_t word_lo = 0, word_hi = 0;
+  if (!d->tasks.empty()) {
+    int64_t mx = -1;
+    for (const TaskRec &r : d->tasks) mx = std::max(mx, r.cursor0);
+    word_hi = (uint64_t)(mx + 1);
+    if (c.partitioned) {
+      word_lo = part_start[task_begin];
+    } else if (task_begin >= 2) {
+      // task a reads no word below offset(point a-2) - 31 when sync_start(point a-1) >
+      // boundary(point a-2) (reading Z9, enforced by the encoder); else start at 0.
+      int64_t ss1, bi1, ss2, bi2;
+      point_span(c, task_begin - 1, &ss1, &bi1);
+      point_span(c, task_begin - 2, &ss2, &bi2);
+      if (ss1 > bi2 && c.offset[task_begin - 2] >= kLanes - 1) word_lo = c.offset[task_begin - 2] - (kLanes - 1);
+    }
+  }
+  word_lo &= ~(uint64_t)(kChunkWords - 1);
+  word_hi = ceil_div(std::max(word_hi, word_lo + 1), kChunkWords) * kChunkWords;
+  if (for_gpu && word_hi - word_lo >= (1ull << 31)) return RECOIL_E_UNSUPPORTED;  // 32-bit slice cursor
+  p.word_lo = word_lo;
+  p.word_count = word_hi - word_lo;
+  for (TaskRec &r : d->tasks) {
+    r.cursor0 -= (int64_t)word_lo;
+    if (r.end_cursor != kNoEndCheck) r.end_cursor -= (int64_t)word_lo;
+  }
+  if (!d->tasks.empty()) {
+    p.out_lo = d->tasks.front().commit_lo;
+    p.out_hi = d->tasks.back().commit_hi + 1;
+  }
+  p.out_base = p.out_lo & ~(uint64_t)(kBlockBytes - 1);
+  uint64_t write_end = p.out_hi;
+  for (const TaskRec &r : d->tasks) write_end = std::max(write_end, r.write_hi);
+  p.out_count = ((write_end + 15) & ~15ull) - p.out_base;
+  d->lut_off = 16;
+  d->finals_off = align16(d->lut_off + 4 * d->lut.size());
+  d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
+  p.workspace_bytes = align16(d->tasks_off + sizeof(TaskRec) * d->tasks.size());
+  p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);
+  return RECOIL_OK;
+}
+
+}  // namespace recoil
+
+using namespace recoil;
+
+extern "C" int recoil_decoder_create(const uint8_t *container, uint64_t len, uint64_t task_begin,
+                                     uint64_t task_end, recoil_decoder **out) {
+  if (!container || !out) return RECOIL_E_ARG;
+  *out = nullptr;
+  try {
+    Decoder *d = new Decoder();
+    int rc = build_decoder(container, len, task_begin, task_end, d, true);
+    if (rc) {
+      delete d;
+      return rc;
+    }
+    *out = reinterpret_cast<recoil_decoder *>(d);
+    return RECOIL_OK;
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}
+
+extern "C" int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan) {
+  if (!dec || !plan) return RECOIL_E_ARG;
+  *plan = reinterpret_cast<const Decoder *>(dec)->plan;
+  return RECOIL_OK;
+}
+
+extern "C" void recoil_decoder_destroy(recoil_decoder *dec) { delete reinterpret_cast<Decoder *>(dec); }
+
+extern "C" int recoil_shard_plan(const uint8_t *container, uint64_t len, uint32_t n_shards,
+                                 uint64_t *bounds) {
+  if (!container || !bounds || n_shards < 1) return RECOIL_E_ARG;
+  try {
+    Container c;
+    int rc = parse_container(container, len, &c);
+    if (rc) return rc;
+    // commit_lo of every task; shard d starts at the first task whose commit_lo >= d N / D
+    std::vector<uint64_t> lo(c.M);
+    for (uint64_t t = 0; t < c.M; ++t) {
+      if (c.partitioned) {
+        lo[t] = kLanes * (t * c.G / c.M);
+      } else if (t == 0) {
+        lo[t] = 0;
+      } else {
+        int64_t ss, bi;
+        point_span(c, t - 1, &ss, &bi);
+        lo[t] = (uint64_t)ss;
+      }
+    }
+    bounds[0] = 0;
+    for (uint32_t s = 1; s < n_shards; ++s) {
+      uint64_t target = ceil_div((uint64_t)s * c.N, n_shards);
+      uint64_t b = (uint64_t)(std::lower_bound(lo.begin(), lo.end(), target) - lo.begin());
+      bounds[s] = std::max(bounds[s - 1], std::min<uint64_t>(b, c.M));
+    }
+    bounds[n_shards] = c.M;
+    return RECOIL_OK;
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}

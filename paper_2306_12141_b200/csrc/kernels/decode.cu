@@ -1,0 +1,513 @@
+// decode.cu -- the Recoil decode kernel for sm_100a and its C-ABI entry points
+// (recoil_decoder_upload / recoil_decode / recoil_decoder_status /
+// recoil_decode_occupancy / recoil_decoder_launches).
+//
+// One warp per split task (a 32-way interleaved group "naturally fits
+// into a GPU warp"); lane j is interleaved decoder D_j.  Per symbol group g
+// (32 symbols, one per lane), top-down:
+//   refill  (Eq. 4): lanes with x < L read one 16-bit word, in
+//           decreasing lane order: m = ballot(x < L), lane j reads
+//           word[cursor - popc(m & lanes_above_j)], cursor -= popc(m);
+//   decode  (Eq. 2): e = lut[x mod 2^n] from the shared-memory
+//           packed LUT (s | bias << 8 | f << 20), x = f (x >> n) + bias.
+// Synchronization Phase: a lane is initialised with its 16-bit
+// anchor state in its anchor group, immediately before its first read;
+// uninitialised lanes hold 0xFFFFFFFF (never < L, so they never read) and
+// their decodes are discarded.  The Decoding and Cross-Boundary phases
+// are the same loop with every lane initialised, down to the
+// group of the task's commit_lo; that steady state runs as fully unrolled
+// 16-group blocks (one 512-byte output block each) with no per-group branch.
+//
+// Memory path: the words come from a per-warp 2 KB shared-memory ring filled
+// by warp-cooperative 16-byte cp.async loads (256 words per chunk, two chunks
+// of look-ahead, checked every 8 groups since 8 groups consume <= 256 words);
+// task records stream in by cp.async one task ahead, tasks are handed out by
+// an atomic counter (persistent warps); decoded bytes are staged per output
+// block in shared memory and leave as one 16-byte store per lane (byte stores
+// only in the one 16-byte chunk per commit edge).  All shared accesses use
+// 32-bit shared-window addresses (inline PTX) computed once per warp.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "../recoil_internal.h"
+
+namespace recoil {
+namespace dev {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kThreads = kWarpsPerBlock * 32;
+constexpr int kMinBlocksPerSM = 5;  // 40 resident warps/SM (<= 48 registers)
+constexpr int kRingChunks = 4;
+constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
+constexpr uint32_t kRingBytes = 2 * kRingWords;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+struct Params {
+  const uint32_t *lut;
+  const uint32_t *finals;
+  const TaskRec *tasks;
+  DeviceStatus *status;
+  const uint16_t *words;  // slice base (stream word word_lo)
+  uint8_t *out;           // symbol out_base
+  uint64_t out_base;
+  int32_t n_chunks;       // slice words / 256
+  uint32_t n_tasks;
+  // Runtime constants, opaque to ptxas, that keep some steady-state work on the
+  // FMA pipe (IMAD) instead of the ALU pipe, which is the busiest one:
+  int32_t neg2;           // -2: cursor arithmetic as IMAD instead of IADD3
+  uint32_t k4096;         // 2^12: bias = (e * 2^12) >> 20 as IMAD + SHF instead of SHF + LOP3
+};
+
+// Dynamic shared memory: [pad to 2 KB][rings 8 x 2 KB][stages 8 x 512 B][records 8 x 2 x 176 B][LUT 2^n x 4 B]
+constexpr uint32_t kStageOff = kWarpsPerBlock * kRingBytes;
+constexpr uint32_t kRecOff = kStageOff + kWarpsPerBlock * kBlockBytes;
+constexpr uint32_t kLutOff = kRecOff + kWarpsPerBlock * 2 * sizeof(TaskRec);
+static_assert(kLutOff % 16 == 0, "LUT alignment");
+constexpr uint32_t kPadBytes = 2048;
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stg_v4(void *p, int4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_gt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_gt;" : "=r"(m));
+  return m;
+}
+
+struct Warp {
+  const Params *p;
+  uint32_t ring32;   // 2 KB-aligned shared address of this warp's word ring
+  uint32_t stage32;  // this warp's 512-B staging block + lane
+  uint32_t lut32;
+  uint32_t gt;       // lanes above this one
+  int lane;
+  int rot;           // ring rotation: chunk c lives in slot (c + rot) & 3
+  int cursor2;       // 2 x (slice-relative index of the next word to read) + 512 rot
+  int cchunk;        // cursor2 >> 9 at the last window check (rotated chunk index)
+
+  // a7: warp-cooperative prefetch of rotated chunk cr (256 words = 32 lanes x 16 B)
+  __device__ __forceinline__ void issue_chunk(int cr) {
+    const int c = cr - rot;
+    if (c >= 0 && c < p->n_chunks)
+      cp_async16(ring32 + (uint32_t)(cr & (kRingChunks - 1)) * (2 * kChunkWords) + 16 * lane,
+                 p->words + (size_t)c * kChunkWords + lane * 8);
+    cp_commit();
+  }
+  // Keep chunks cchunk and cchunk-1 complete and cchunk-2 in flight.  8 groups
+  // consume at most 256 words, so one check covers the next 8 groups.
+  __device__ __forceinline__ void window_check() {
+    if ((cursor2 >> 9) != cchunk) {
+      --cchunk;
+      issue_chunk(cchunk - 2);
+      cp_wait<1>();
+      __syncwarp();
+    }
+  }
+  // Eq. 4 with the interleaved read order: lanes below read after the
+  // lanes above them.  pre = needing lanes above this one (POPC); the warp total
+  // comes from REDUX, which runs outside the LDS/POPC pipe.
+  __device__ __forceinline__ uint32_t refill(uint32_t x) {
+    const bool need = x < kL;
+    const uint32_t m = __ballot_sync(kFull, need);
+    const int pre = __popc(m & gt);
+    const int total = (int)__reduce_add_sync(kFull, (uint32_t)need);
+    const uint32_t w = lds_u16(ring32 | ((uint32_t)(cursor2 + pre * p->neg2) & (kRingBytes - 2)));
+    cursor2 += total * p->neg2;
+    return need ? x * 65536u + w : x;
+  }
+  // Eq. 2 with the packed LUT; stages the symbol byte of group slot k (= g mod 16)
+  template <int NB>
+  __device__ __forceinline__ uint32_t decode(uint32_t x, uint32_t k) {
+    const uint32_t e = lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
+    sts_u8(stage32 + k * 32, e);
+    return (e >> 20) * (x >> NB) + ((e * p->k4096) >> 20);  // f (x >> n) + bias
+  }
+  // a8: write output block b: every 16-B chunk inside [wlo, whi) as one store
+  __device__ __forceinline__ void flush(int b, uint64_t wlo, uint64_t whi) {
+    __syncwarp();
+    const uint64_t c0 = (uint64_t)(uint32_t)b * kBlockBytes + 16 * lane;
+    if (c0 >= wlo && c0 + 16 <= whi) stg_v4(p->out + (c0 - p->out_base), lds_v4(stage32 + 15 * lane));
+    __syncwarp();
+  }
+};
+
+// One group step.  SYNC: Synchronization Phase logic -- lane j is
+// initialised with its anchor state in its anchor group, before its read;
+// uninitialised lanes keep x = 0xFFFFFFFF and their decodes are discarded.
+template <int NB, bool SYNC>
+__device__ __forceinline__ uint32_t step(Warp &w, uint32_t x, int g, int k, int init_group, uint32_t state) {
+  if (SYNC && g == init_group) x = state;
+  x = w.refill(x);
+  const uint32_t xn = w.decode<NB>(x, (uint32_t)k);
+  return (SYNC && g > init_group) ? 0xFFFFFFFFu : xn;
+}
+
+// Groups g .. g_end of one 16-group output block (g_end <= g, same block),
+// entered at slot g & 15 (Duff's device) and left after slot g_end & 15.
+template <int NB, bool SYNC>
+__device__ __forceinline__ uint32_t run_part(Warp &w, uint32_t x, int g, int g_end, int init_group,
+                                             uint32_t state) {
+  const int gb = g & ~15, k1 = g_end & 15;
+  w.window_check();
+#define RECOIL_STEP(K)                                                  \
+  x = step<NB, SYNC>(w, x, gb + K, K, init_group, state);               \
+  if (k1 == K) break;
+  switch (g & 15) {
+    case 15: RECOIL_STEP(15) [[fallthrough]];
+    case 14: RECOIL_STEP(14) [[fallthrough]];
+    case 13: RECOIL_STEP(13) [[fallthrough]];
+    case 12: RECOIL_STEP(12) [[fallthrough]];
+    case 11: RECOIL_STEP(11) [[fallthrough]];
+    case 10: RECOIL_STEP(10) [[fallthrough]];
+    case 9: RECOIL_STEP(9) [[fallthrough]];
+    case 8:
+      RECOIL_STEP(8)
+      w.window_check();  // entered at slot >= 8: re-check before slots 7..0
+      [[fallthrough]];
+    case 7: RECOIL_STEP(7) [[fallthrough]];
+    case 6: RECOIL_STEP(6) [[fallthrough]];
+    case 5: RECOIL_STEP(5) [[fallthrough]];
+    case 4: RECOIL_STEP(4) [[fallthrough]];
+    case 3: RECOIL_STEP(3) [[fallthrough]];
+    case 2: RECOIL_STEP(2) [[fallthrough]];
+    case 1: RECOIL_STEP(1) [[fallthrough]];
+    default: RECOIL_STEP(0)
+  }
+#undef RECOIL_STEP
+  return x;
+}
+
+// A whole 16-group block with every lane initialised: no branch per group.
+template <int NB>
+__device__ __forceinline__ uint32_t run_block(Warp &w, uint32_t x) {
+  w.window_check();
+#pragma unroll
+  for (int k = 15; k >= 8; --k) {
+    x = w.refill(x);
+    x = w.decode<NB>(x, k);
+  }
+  w.window_check();
+#pragma unroll
+  for (int k = 7; k >= 0; --k) {
+    x = w.refill(x);
+    x = w.decode<NB>(x, k);
+  }
+  return x;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kernel(const Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // the dynamic window starts 1 KB-aligned; the rings need 2 KB alignment
+  const uint32_t base32 = (smem_addr(smem_raw) + kPadBytes - 1) & ~(kPadBytes - 1);
+  unsigned char *const smem = smem_raw + (base32 - smem_addr(smem_raw));
+  const uint32_t lut_words = 1u << NB;
+
+  // a2: stage the packed LUT in shared memory (per block)
+  {
+    unsigned char *lut_g = smem + kLutOff;
+    if (NB >= 2) {
+      for (uint32_t i = threadIdx.x; i < lut_words / 4; i += kThreads)
+        reinterpret_cast<int4 *>(lut_g)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+    } else if (threadIdx.x < lut_words) {
+      reinterpret_cast<uint32_t *>(lut_g)[threadIdx.x] = p.lut[threadIdx.x];
+    }
+  }
+  __syncthreads();
+
+  Warp w;
+  w.p = &p;
+  w.lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  w.ring32 = base32 + warp * kRingBytes;
+  w.stage32 = base32 + kStageOff + warp * kBlockBytes + w.lane;
+  w.lut32 = base32 + kLutOff;
+  w.gt = lanemask_gt();
+  w.rot = 0;
+  w.cchunk = 2;  // first task: any stale slot
+  const uint32_t rec32 = base32 + kRecOff + warp * 2 * sizeof(TaskRec);
+  const unsigned char *rec_g = smem + kRecOff + warp * 2 * sizeof(TaskRec);
+  const int lane = w.lane;
+
+  // a3: persistent warps.  The first wave of task ids is static; afterwards a
+  // warp takes the next id from an atomic counter shortly before it finishes
+  // its current task (two blocks ahead: the atomic's latency hides behind them)
+  // and streams that record into shared memory by cp.async.  Taking ids late
+  // matters: warps of one SM run at very different speeds under the
+  // oldest/highest-priority issue policy, so an id reserved early by a slow
+  // warp would become the kernel's tail.
+  const uint32_t first_wave = gridDim.x * kWarpsPerBlock;
+  auto issue_task = [&](uint32_t t, int buf) {
+    if (t < p.n_tasks && lane < (int)(sizeof(TaskRec) / 16))
+      cp_async16(rec32 + buf * sizeof(TaskRec) + 16 * lane,
+                 reinterpret_cast<const char *>(&p.tasks[t]) + 16 * lane);
+    cp_commit();
+  };
+  uint32_t t = blockIdx.x * kWarpsPerBlock + warp;
+  int buf = 0;
+  if (t < p.n_tasks) issue_task(t, 0);
+  while (t < p.n_tasks) {
+    cp_wait<0>();  // this task's record (and any stale window copy) has landed
+    __syncwarp();
+    const TaskRec &r = *reinterpret_cast<const TaskRec *>(rec_g + buf * sizeof(TaskRec));
+    const int32_t start_group = r.start_group;
+    const uint64_t lo = r.commit_lo, whi = r.write_hi;
+    const int64_t end_cursor = r.end_cursor;
+    const uint32_t task_id = r.task_id;
+    const uint32_t lw = r.lanes[lane];
+    const uint32_t state = r.finals_idx == kNoFinals ? (lw & 0xFFFFu) : p.finals[r.finals_idx * 32 + lane];
+    const int32_t init_group = start_group - (int32_t)(lw >> 16);
+    const int cursor0 = (int)r.cursor0;
+    __syncwarp();
+    // next task: 0 = not asked, 1 = atomic in flight, 2 = record prefetch issued
+    int next_state = 0;
+    uint32_t t_after = 0, t_next = p.n_tasks;
+    auto next_task_step = [&]() {
+      if (next_state == 0) {
+        if (lane == 0) t_after = first_wave + atomicAdd(&p.status->next_task, 1u);
+        next_state = 1;
+      } else if (next_state == 1) {
+        t_next = __shfl_sync(kFull, t_after, 0);
+        issue_task(t_next, buf ^ 1);
+        next_state = 2;
+      }
+    };
+
+    // a7: word window.  The previous task may have one chunk copy in flight into
+    // slot (cchunk - 2) & 3; rotate so that slot is this task's 4th chunk, which
+    // is only issued after the first wait below has retired the stale copy.
+    const int stale_slot = (w.cchunk - 2) & 3;
+    w.rot = (stale_slot - (cursor0 >> 8) + 3) & 3;
+    w.cursor2 = 2 * cursor0 + 512 * w.rot;
+    w.cchunk = w.cursor2 >> 9;
+    w.issue_chunk(w.cchunk);
+    w.issue_chunk(w.cchunk - 1);
+    w.issue_chunk(w.cchunk - 2);
+    cp_wait<1>();
+    __syncwarp();
+
+    const int32_t lo_group = (int32_t)(lo >> 5);
+    const uint64_t wlo = (uint64_t)lo_group * kLanes;
+    int32_t min_init = init_group;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) min_init = min(min_init, __shfl_xor_sync(kFull, min_init, o));
+    const int32_t g_sync_end = max(min_init, lo_group);
+
+    uint32_t x = 0xFFFFFFFFu;  // uninitialised: never < L
+    int32_t g = start_group;
+
+    // a4: Synchronization Phase -- groups where some lane is still uninitialised
+    while (g >= g_sync_end) {
+      const int gb = g & ~15, ge = max(gb, g_sync_end);
+      x = run_part<NB, true>(w, x, g, ge, init_group, state);
+      if (ge == gb) w.flush(gb >> 4, wlo, whi);
+      g = ge - 1;
+    }
+    // a5 + a6: Decoding Phase and Cross-Boundary Phase (all lanes initialised)
+    while (g >= lo_group) {
+      const int gb = g & ~15, ge = max(gb, lo_group);
+      if ((g & 15) == 15 && ge == gb)
+        x = run_block<NB>(w, x);
+      else
+        x = run_part<NB, false>(w, x, g, ge, 0, 0);
+      w.flush(gb >> 4, wlo, whi);
+      g = ge - 1;
+      if (g - lo_group < 48) next_task_step();
+    }
+    while (next_state < 2) next_task_step();
+
+    // a9: integrity -- a task that reaches its codec's start must end in the
+    // stack-property end state: cursor one below the codec's first word,
+    // every initialised lane back at L.
+    const int cursor = (w.cursor2 - 512 * w.rot) >> 1;
+    bool bad_end = false;
+    const bool under = cursor < -1;
+    if (end_cursor != kNoEndCheck) {
+      const bool lane_ok = (init_group < lo_group) || x == kL;
+      bad_end = (cursor != (int)end_cursor) || !__all_sync(kFull, lane_ok);
+    }
+    if (lane == 0 && (bad_end || under)) {
+      atomicOr(&p.status->flags, (under ? 1u : 0u) | (bad_end ? 2u : 0u));
+      atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
+    }
+    t = t_next;
+    buf ^= 1;
+  }
+  cp_wait<0>();
+}
+
+using KernelFn = void (*)(const Params);
+static KernelFn kernel_for(uint32_t nbits) {
+  switch (nbits) {
+    case 1: return recoil_decode_kernel<1>;
+    case 2: return recoil_decode_kernel<2>;
+    case 3: return recoil_decode_kernel<3>;
+    case 4: return recoil_decode_kernel<4>;
+    case 5: return recoil_decode_kernel<5>;
+    case 6: return recoil_decode_kernel<6>;
+    case 7: return recoil_decode_kernel<7>;
+    case 8: return recoil_decode_kernel<8>;
+    case 9: return recoil_decode_kernel<9>;
+    case 10: return recoil_decode_kernel<10>;
+    case 11: return recoil_decode_kernel<11>;
+    case 12: return recoil_decode_kernel<12>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace dev
+
+static size_t smem_bytes(uint32_t nbits) { return dev::kPadBytes + dev::kLutOff + ((size_t)4 << nbits); }
+
+static int configure(dev::KernelFn fn, uint32_t nbits) {
+  cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared);
+  cudaError_t e2 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(nbits));
+  return (e1 == cudaSuccess && e2 == cudaSuccess) ? RECOIL_OK : RECOIL_E_CUDA;
+}
+
+static int occupancy(uint32_t nbits, int *blocks_per_sm) {
+  dev::KernelFn fn = dev::kernel_for(nbits);
+  if (!fn) return RECOIL_E_ARG;
+  int rc = configure(fn, nbits);
+  if (rc) return rc;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, dev::kThreads, smem_bytes(nbits)) !=
+      cudaSuccess)
+    return RECOIL_E_CUDA;
+  return RECOIL_OK;
+}
+
+}  // namespace recoil
+
+using namespace recoil;
+
+extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uint16_t *d_words, void *stream) {
+  if (!dec || !d_workspace || !d_words) return RECOIL_E_ARG;
+  Decoder *d = reinterpret_cast<Decoder *>(dec);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(d_workspace);
+  const recoil_plan &p = d->plan;
+  if (cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return RECOIL_E_CUDA;
+  if (!d->lut.empty() && cudaMemcpyAsync(ws + d->lut_off, d->lut.data(), 4 * d->lut.size(),
+                                         cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (!d->finals.empty() && cudaMemcpyAsync(ws + d->finals_off, d->finals.data(), 4 * d->finals.size(),
+                                            cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (!d->tasks.empty() && cudaMemcpyAsync(ws + d->tasks_off, d->tasks.data(), sizeof(TaskRec) * d->tasks.size(),
+                                           cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  uint64_t have = d->c.B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c.B - p.word_lo) : 0;
+  if (have && cudaMemcpyAsync(d_words, d->c.words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
+                  cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (p.word_count > have && cudaMemsetAsync(d_words + have, 0, 2 * (p.word_count - have), s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  return RECOIL_OK;
+}
+
+extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint16_t *d_words, uint8_t *d_out,
+                             void *stream) {
+  if (!dec || !d_workspace || !d_words) return RECOIL_E_ARG;
+  Decoder *d = reinterpret_cast<Decoder *>(dec);
+  const recoil_plan &pl = d->plan;
+  if (!d_out && pl.out_hi > pl.out_lo) return RECOIL_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(d_workspace);
+  if (cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return RECOIL_E_CUDA;  // status + task counter
+  if (pl.n_tasks == 0) return RECOIL_OK;
+  if (d->single_symbol >= 0) {  // f = 2^n: every state decodes to the one symbol (Eq. 2 identity)
+    return cudaMemsetAsync(d_out + (pl.out_lo - pl.out_base), d->single_symbol, pl.out_hi - pl.out_lo, s) ==
+                   cudaSuccess
+               ? RECOIL_OK
+               : RECOIL_E_CUDA;
+  }
+  if (d->blocks_per_sm == 0) {
+    int rc = occupancy(pl.prob_bits, &d->blocks_per_sm);
+    if (rc) return rc;
+    int dev_id = 0;
+    if (cudaGetDevice(&dev_id) != cudaSuccess ||
+        cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
+      return RECOIL_E_CUDA;
+    if (d->blocks_per_sm < 1) return RECOIL_E_CUDA;
+  }
+  dev::Params prm;
+  prm.lut = reinterpret_cast<const uint32_t *>(ws + d->lut_off);
+  prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
+  prm.tasks = reinterpret_cast<const TaskRec *>(ws + d->tasks_off);
+  prm.status = reinterpret_cast<DeviceStatus *>(ws);
+  prm.words = d_words;
+  prm.out = d_out;
+  prm.out_base = pl.out_base;
+  prm.n_chunks = (int32_t)(pl.word_count / kChunkWords);
+  prm.n_tasks = pl.n_tasks;
+  prm.neg2 = -2;
+  prm.k4096 = 4096;
+  const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
+  const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
+  dev::kernel_for(pl.prob_bits)<<<grid, dev::kThreads, smem_bytes(pl.prob_bits), s>>>(prm);
+  return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
+}
+
+extern "C" int recoil_decoder_status(recoil_decoder *dec, const void *d_workspace, void *stream, uint64_t *bad) {
+  if (!dec || !d_workspace) return RECOIL_E_ARG;
+  DeviceStatus st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(&st, d_workspace, sizeof(st), cudaMemcpyDeviceToHost, s) != cudaSuccess) return RECOIL_E_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return RECOIL_E_CUDA;
+  if (bad) *bad = st.bad_task ? (uint64_t)(0xFFFFFFFFu - st.bad_task) : UINT64_MAX;
+  if (st.flags & 1u) return RECOIL_E_UNDERFLOW;
+  if (st.flags & 2u) return RECOIL_E_SYNC;
+  return RECOIL_OK;
+}
+
+extern "C" int recoil_decoder_launches(const recoil_decoder *dec) {
+  if (!dec) return RECOIL_E_ARG;
+  const Decoder *d = reinterpret_cast<const Decoder *>(dec);
+  return (d->plan.n_tasks == 0 || d->single_symbol >= 0) ? 0 : 1;
+}
+
+extern "C" int recoil_decode_occupancy(int device, uint32_t nbits, int *warps_per_sm, int *sm_count) {
+  if (nbits < 1 || nbits > kMaxGpuProbBits) return RECOIL_E_ARG;
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
+  int per_sm = 0, sms = 0;
+  int rc = occupancy(nbits, &per_sm);
+  cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaSetDevice(prev);
+  if (rc) return rc;
+  if (e2 != cudaSuccess) return RECOIL_E_CUDA;
+  if (warps_per_sm) *warps_per_sm = per_sm * dev::kWarpsPerBlock;
+  if (sm_count) *sm_count = sms;
+  return RECOIL_OK;
+}

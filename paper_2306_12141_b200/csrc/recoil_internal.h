@@ -1,0 +1,90 @@
+// recoil_internal.h -- internal types of librecoil (host C++ and CUDA).
+// Not part of the ABI; the ABI is include/recoil.h.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "recoil.h"
+
+namespace recoil {
+
+constexpr uint32_t kLanes = 32;          // W (tab:rans_params P:419)
+constexpr uint32_t kL = 1u << 16;        // L
+constexpr uint32_t kWordBits = 16;       // b
+constexpr uint32_t kChunkWords = 256;    // device word-window chunk: 32 lanes x 16 B
+constexpr uint32_t kBlockBytes = 512;    // device output block: 16 groups x 32 symbols
+constexpr uint32_t kMaxGpuProbBits = 12; // packed u32 LUT limit
+constexpr uint32_t kNoFinals = 0xFFFFFFFFu;
+constexpr int64_t kNoEndCheck = INT64_MIN;
+
+// Parsed container of either kind. Recoil: M tasks, M-1 split points.
+// Partitioned: M partitions (tasks), no points.
+struct Container {
+  bool partitioned = false;
+  uint32_t n = 0, W = 0, M = 0;
+  uint64_t N = 0, B = 0, G = 0;
+  uint32_t f[256] = {0};
+  std::vector<uint32_t> finals;   // Recoil: W final states; partitioned: M x W
+  std::vector<uint64_t> offset;   // Recoil: M-1 split offsets (word index of the boundary event)
+  std::vector<uint64_t> maxg;     // Recoil: M-1 anchor (max) group IDs
+  std::vector<uint16_t> state;    // Recoil: (M-1) x W anchor states (< L)
+  std::vector<uint16_t> gdiff;    // Recoil: (M-1) x W group differences to the anchor
+  std::vector<uint64_t> part_words; // partitioned: M word counts
+  const uint8_t *words = nullptr; // B little-endian u16
+  uint64_t header_bytes = 0, meta_bytes = 0, total_bytes = 0;
+};
+
+int parse_container(const uint8_t *c, uint64_t len, Container *out);
+// Serialise a Recoil container (offset/maxg/state/gdiff/finals/f from `c`,
+// words from `words` (B little-endian u16 bytes)).  out == nullptr: size only.
+int write_recoil_container(const Container &c, const uint8_t *words, uint8_t *out, uint64_t *len);
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Anchor span of split point k: sync start (min anchor index) and boundary index (max).
+void point_span(const Container &c, uint64_t k, int64_t *sync_start, int64_t *bidx);
+
+// ---------------------------------------------------------------------------
+// Device task record: 176 B, 16-B aligned.
+// ---------------------------------------------------------------------------
+struct alignas(16) TaskRec {
+  int64_t cursor0;      // slice-relative word index of the task's first read
+  int64_t end_cursor;   // slice-relative cursor the task must end at, or kNoEndCheck
+  uint64_t commit_lo;   // first committed symbol (absolute)
+  uint64_t commit_hi;   // last committed symbol (absolute, inclusive)
+  uint64_t write_hi;    // GPU writes the 16-B chunks inside [32 group(commit_lo), write_hi):
+                        // every symbol there is decoded by this task after it is synchronised
+  int32_t start_group;  // group of the first decode step
+  uint32_t finals_idx;  // kNoFinals: lanes[] low 16 bits are the init states; else 32 u32 states
+  uint32_t task_id;     // container task index (error reporting)
+  uint32_t pad[3];
+  uint32_t lanes[32];   // (state16 | diff16 << 16), diff = start_group - init_group
+};
+static_assert(sizeof(TaskRec) == 192, "TaskRec layout");
+
+struct DeviceStatus {   // first 16 B of the workspace, zeroed before every decode
+  uint32_t flags;       // bit 0 underflow, bit 1 end-state mismatch
+  uint32_t bad_task;    // atomicMax of (0xFFFFFFFF - failing task id); 0 = none
+  uint32_t next_task;   // persistent-warp task counter
+  uint32_t pad;
+};
+
+// Host-side decode plan (the recoil_decoder handle).
+struct Decoder {
+  Container c;
+  recoil_plan plan{};
+  std::vector<uint32_t> lut;       // 2^n packed entries: s | bias << 8 | f << 20
+  std::vector<uint32_t> finals;    // K x 32 u32 states referenced by finals_idx
+  std::vector<TaskRec> tasks;
+  uint64_t lut_off = 0, finals_off = 0, tasks_off = 0;  // workspace byte offsets
+  int single_symbol = -1;          // >= 0: the model has one symbol (f = 2^n): decode = fill
+  int blocks_per_sm = 0, sm_count = 0;  // launch geometry (occupancy API), cached
+};
+
+int build_decoder(const uint8_t *c, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
+                  bool for_gpu);
+void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint32_t> *lut);
+
+
+}  // namespace recoil

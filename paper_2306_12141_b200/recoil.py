@@ -1,0 +1,296 @@
+"""Thin ctypes binding of librecoil.so (include/recoil.h).  Argument marshalling only:
+every step of the decode path runs in the library (host C++ for encode/metadata,
+sm_100a CUDA kernels for decode).  There is no Python or CPU fallback: if the
+library is missing or fails to load, every call raises.
+
+Function names equal the C ABI names.  Host buffers are numpy arrays / bytes;
+device buffers are torch CUDA tensors (PyTorch supplies device memory and
+streams only).  Errors raise ``RecoilError`` carrying the RECOIL_E_* code.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librecoil.so")
+_lib = None
+
+RECOIL_OK = 0
+ERRORS = {
+    -1: "RECOIL_E_ARG", -2: "RECOIL_E_EMPTY", -3: "RECOIL_E_ALPHABET", -4: "RECOIL_E_ZERO_FREQ",
+    -5: "RECOIL_E_OVERFLOW", -6: "RECOIL_E_BAD_MAGIC", -7: "RECOIL_E_VERSION", -8: "RECOIL_E_TRUNCATED",
+    -9: "RECOIL_E_INCONSISTENT", -10: "RECOIL_E_UNDERFLOW", -11: "RECOIL_E_SYNC", -12: "RECOIL_E_CUDA",
+    -13: "RECOIL_E_NOMEM", -14: "RECOIL_E_BUFFER", -15: "RECOIL_E_UNSUPPORTED",
+}
+globals().update({v: k for k, v in ERRORS.items()})
+
+EXPORTS = [
+    "recoil_strerror", "recoil_build_model", "recoil_encode", "recoil_combine_splits", "recoil_inspect",
+    "recoil_partitioned_encode", "recoil_decoder_create", "recoil_decoder_plan", "recoil_decoder_upload",
+    "recoil_decode", "recoil_decoder_status", "recoil_decoder_launches", "recoil_decoder_destroy",
+    "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu",
+]
+
+
+class RecoilError(RuntimeError):
+    def __init__(self, rc: int, what: str = ""):
+        name = ERRORS.get(rc, str(rc))
+        super().__init__(f"{what}: {name}" if what else name)
+        self.rc = rc
+
+
+class recoil_info(ctypes.Structure):
+    _fields_ = [("n_symbols", ctypes.c_uint64), ("n_words", ctypes.c_uint64), ("n_splits", ctypes.c_uint32),
+                ("prob_bits", ctypes.c_uint32), ("lanes", ctypes.c_uint32), ("partitioned", ctypes.c_uint32),
+                ("header_bytes", ctypes.c_uint64), ("meta_bytes", ctypes.c_uint64),
+                ("word_bytes", ctypes.c_uint64), ("total_bytes", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class recoil_plan(ctypes.Structure):
+    _fields_ = [("task_begin", ctypes.c_uint64), ("task_end", ctypes.c_uint64), ("n_tasks", ctypes.c_uint32),
+                ("prob_bits", ctypes.c_uint32), ("word_lo", ctypes.c_uint64), ("word_count", ctypes.c_uint64),
+                ("out_lo", ctypes.c_uint64), ("out_hi", ctypes.c_uint64), ("out_base", ctypes.c_uint64),
+                ("out_count", ctypes.c_uint64), ("workspace_bytes", ctypes.c_uint64),
+                ("upload_bytes", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def load(path: str = LIB_PATH):
+    """Load librecoil.so; raises if it is missing (build with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"librecoil.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    sig = {
+        "recoil_strerror": (ctypes.c_char_p, [i32]),
+        "recoil_build_model": (i32, [P, u32, P]),
+        "recoil_encode": (i32, [P, u64, P, u32, u32, P, P]),
+        "recoil_combine_splits": (i32, [P, u64, u32, P, P]),
+        "recoil_inspect": (i32, [P, u64, P]),
+        "recoil_partitioned_encode": (i32, [P, u64, P, u32, u32, P, P]),
+        "recoil_decoder_create": (i32, [P, u64, u64, u64, P]),
+        "recoil_decoder_plan": (i32, [P, P]),
+        "recoil_decoder_upload": (i32, [P, P, P, P]),
+        "recoil_decode": (i32, [P, P, P, P, P]),
+        "recoil_decoder_status": (i32, [P, P, P, P]),
+        "recoil_decoder_launches": (i32, [P]),
+        "recoil_decoder_destroy": (None, [P]),
+        "recoil_decode_occupancy": (i32, [i32, u32, P, P]),
+        "recoil_shard_plan": (i32, [P, u64, u32, P]),
+        "recoil_decode_cpu": (i32, [P, u64, P, u32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str = "") -> int:
+    if rc < 0:
+        raise RecoilError(rc, what)
+    return rc
+
+
+def _u8(buf) -> np.ndarray:
+    if isinstance(buf, np.ndarray):
+        return np.ascontiguousarray(buf.reshape(-1).view(np.uint8))
+    return np.frombuffer(memoryview(buf), dtype=np.uint8)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data if a.size else None
+
+
+def _freqs(f) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(f, dtype=np.uint32).reshape(256))
+
+
+def recoil_strerror(rc: int) -> str:
+    return load().recoil_strerror(rc).decode()
+
+
+def recoil_build_model(hist, prob_bits: int) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.uint64).reshape(256))
+    f = np.zeros(256, dtype=np.uint32)
+    _check(load().recoil_build_model(h.ctypes.data, prob_bits, f.ctypes.data), "recoil_build_model")
+    return f
+
+
+def _sized(fn, what, *args) -> np.ndarray:
+    n = ctypes.c_uint64(0)
+    _check(fn(*args, None, ctypes.byref(n)), what)
+    out = np.empty(n.value, dtype=np.uint8)
+    rc = fn(*args, out.ctypes.data, ctypes.byref(n))
+    if rc == RECOIL_E_BUFFER:
+        out = np.empty(n.value, dtype=np.uint8)
+        rc = fn(*args, out.ctypes.data, ctypes.byref(n))
+    _check(rc, what)
+    return out[: n.value]
+
+
+def recoil_encode(symbols, freqs, prob_bits: int, n_splits: int) -> np.ndarray:
+    """-> container bytes (numpy uint8)."""
+    s = _u8(symbols)
+    return _sized(load().recoil_encode, "recoil_encode", _ptr(s), s.size, _freqs(freqs).ctypes.data, prob_bits,
+                  n_splits)
+
+
+def recoil_partitioned_encode(symbols, freqs, prob_bits: int, n_partitions: int) -> np.ndarray:
+    s = _u8(symbols)
+    return _sized(load().recoil_partitioned_encode, "recoil_partitioned_encode", _ptr(s), s.size,
+                  _freqs(freqs).ctypes.data, prob_bits, n_partitions)
+
+
+def recoil_combine_splits(container, target_splits: int) -> np.ndarray:
+    c = _u8(container)
+    return _sized(load().recoil_combine_splits, "recoil_combine_splits", c.ctypes.data, c.size, target_splits)
+
+
+def recoil_inspect(container) -> dict:
+    c = _u8(container)
+    info = recoil_info()
+    _check(load().recoil_inspect(c.ctypes.data, c.size, ctypes.byref(info)), "recoil_inspect")
+    return info.as_dict()
+
+
+def recoil_shard_plan(container, n_shards: int) -> list[int]:
+    c = _u8(container)
+    b = np.zeros(n_shards + 1, dtype=np.uint64)
+    _check(load().recoil_shard_plan(c.ctypes.data, c.size, n_shards, b.ctypes.data), "recoil_shard_plan")
+    return [int(x) for x in b]
+
+
+def recoil_decode_cpu(container, threads: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    c = _u8(container)
+    N = recoil_inspect(c)["n_symbols"]
+    if out is None:
+        out = np.empty(N, dtype=np.uint8)
+    _check(load().recoil_decode_cpu(c.ctypes.data, c.size, _ptr(out), threads), "recoil_decode_cpu")
+    return out
+
+
+def recoil_decode_occupancy(device: int, prob_bits: int) -> tuple[int, int]:
+    w, s = ctypes.c_int(0), ctypes.c_int(0)
+    _check(load().recoil_decode_occupancy(device, prob_bits, ctypes.byref(w), ctypes.byref(s)),
+           "recoil_decode_occupancy")
+    return w.value, s.value
+
+
+# --- decoder handle ---------------------------------------------------------------------
+
+def recoil_decoder_create(container, task_begin: int = 0, task_end: int = (1 << 64) - 1) -> ctypes.c_void_p:
+    c = _u8(container)
+    h = ctypes.c_void_p()
+    _check(load().recoil_decoder_create(c.ctypes.data, c.size, task_begin, task_end, ctypes.byref(h)),
+           "recoil_decoder_create")
+    return h
+
+
+def recoil_decoder_plan(handle) -> dict:
+    p = recoil_plan()
+    _check(load().recoil_decoder_plan(handle, ctypes.byref(p)), "recoil_decoder_plan")
+    return p.as_dict()
+
+
+def recoil_decoder_upload(handle, d_workspace: int, d_words: int, stream: int) -> None:
+    _check(load().recoil_decoder_upload(handle, d_workspace, d_words, stream), "recoil_decoder_upload")
+
+
+def recoil_decode(handle, d_workspace: int, d_words: int, d_out: int, stream: int) -> None:
+    _check(load().recoil_decode(handle, d_workspace, d_words, d_out, stream), "recoil_decode")
+
+
+def recoil_decoder_status(handle, d_workspace: int, stream: int) -> tuple[int, int | None]:
+    bad = ctypes.c_uint64(0)
+    rc = load().recoil_decoder_status(handle, d_workspace, stream, ctypes.byref(bad))
+    return rc, (None if bad.value == (1 << 64) - 1 else bad.value)
+
+
+def recoil_decoder_launches(handle) -> int:
+    return _check(load().recoil_decoder_launches(handle), "recoil_decoder_launches")
+
+
+def recoil_decoder_destroy(handle) -> None:
+    if handle:
+        load().recoil_decoder_destroy(handle)
+
+
+class GpuDecoder:
+    """Owns a decoder handle plus the torch device buffers of its plan.
+
+    ``container`` must stay alive as long as this object (the handle points into it).
+    """
+
+    def __init__(self, container, device: int = 0, task_begin: int = 0, task_end: int = (1 << 64) - 1,
+                 stream=None):
+        import torch
+        self.container = _u8(container)
+        self.device = torch.device("cuda", device)
+        self.handle = recoil_decoder_create(self.container, task_begin, task_end)
+        self.plan = recoil_decoder_plan(self.handle)
+        p = self.plan
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        self.workspace = torch.empty(max(p["workspace_bytes"], 16), dtype=torch.uint8, device=self.device)
+        self.words = torch.empty(max(p["word_count"], 1), dtype=torch.int16, device=self.device)
+        self.out = torch.empty(max(p["out_count"], 16), dtype=torch.uint8, device=self.device)
+
+    @property
+    def stream_handle(self) -> int:
+        return self.stream.cuda_stream
+
+    def upload(self) -> None:
+        recoil_decoder_upload(self.handle, self.workspace.data_ptr(), self.words.data_ptr(), self.stream_handle)
+
+    def decode(self, out=None) -> None:
+        o = self.out if out is None else out
+        recoil_decode(self.handle, self.workspace.data_ptr(), self.words.data_ptr(), o.data_ptr(),
+                      self.stream_handle)
+
+    def status(self) -> tuple[int, int | None]:
+        return recoil_decoder_status(self.handle, self.workspace.data_ptr(), self.stream_handle)
+
+    def output(self):
+        """Committed symbols [out_lo, out_hi) as a device tensor view."""
+        p = self.plan
+        return self.out[p["out_lo"] - p["out_base"]: p["out_hi"] - p["out_base"]]
+
+    def launches(self) -> int:
+        return recoil_decoder_launches(self.handle)
+
+    def close(self) -> None:
+        recoil_decoder_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.close()
+        except Exception:
+            pass
+
+
+def decode_gpu(container, device: int = 0):
+    """Convenience: full decode on one GPU; returns the device tensor of N symbols
+    (raises RecoilError on a device status error)."""
+    dec = GpuDecoder(container, device)
+    dec.upload()
+    dec.decode()
+    rc, bad = dec.status()
+    if rc:
+        raise RecoilError(rc, f"decode (task {bad})")
+    out = dec.output().clone()
+    dec.close()
+    return out

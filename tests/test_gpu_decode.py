@@ -1,0 +1,198 @@
+"""GPU parity: the sm_100a decode kernel (through the C ABI) vs the oracle.
+
+Every test compares the kernel's output element by element with the oracle's
+decode of the same container (and with the input symbols, which is the plain
+definition of the decode's result).  Tolerance: bit-exact (integer path).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2306_12141_b200 import recoil as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    assert torch.cuda.is_available()
+
+
+def gpu_decode(c, task_begin=0, task_end=(1 << 64) - 1):
+    dec = R.GpuDecoder(c, 0, task_begin, task_end)
+    dec.upload()
+    dec.decode()
+    rc, bad = dec.status()
+    out = dec.output().cpu().numpy()
+    plan = dec.plan
+    dec.close()
+    return rc, bad, out, plan
+
+
+def _check_full(c, sym):
+    rc, bad, out, plan = gpu_decode(c)
+    assert rc == 0, (R.ERRORS.get(rc), bad)
+    assert (plan["out_lo"], plan["out_hi"]) == (0, len(sym))
+    if len(sym) <= 4_000_000:
+        want = oracle.recoil_decode(bytes(c)) if R.recoil_inspect(c)["partitioned"] == 0 \
+            else oracle.partitioned_decode(bytes(c))
+        assert (want == sym).all()
+    mism = np.nonzero(out != sym)[0]
+    assert mism.size == 0, f"{mism.size} mismatches, first at {mism[:5]}"
+
+
+FUZZ = []
+for i, (N, n, M, kind) in enumerate([
+        (1, 11, 1, "exp"), (31, 11, 2, "exp"), (32, 11, 2, "text"), (33, 11, 3, "image"), (511, 11, 4, "exp"),
+        (512, 11, 4, "exp"), (513, 11, 4, "exp"), (5000, 1, 3, "exp"), (5000, 2, 5, "exp"), (20000, 8, 9, "text"),
+        (65536, 11, 16, "exp"), (100000, 12, 33, "image"), (123457, 10, 100, "text"), (300000, 11, 1000, "exp"),
+        (777777, 11, 4096, "text"), (1 << 20, 12, 2176, "image")]):
+    FUZZ.append((N, n, M, kind, 1000 + i))
+
+
+@pytest.mark.parametrize("N,n,M,kind,seed", FUZZ)
+def test_fuzz_vs_oracle(N, n, M, kind, seed):
+    sym = synth.workload(kind, N, seed=seed, lam=float(10 + seed % 190))
+    if n < 8:  # small alphabets for small n
+        sym = (sym % (1 << (n - 1) if n > 1 else 1)).astype(np.uint8) if n <= 2 else sym % 32
+    hist = synth.histogram(sym)
+    f = oracle.build_model(hist, n)
+    c = R.recoil_encode(sym, f, n, M)
+    assert c.tobytes() == oracle.recoil_encode(sym, f, n, M)
+    _check_full(c, sym)
+
+
+def test_single_symbol_fill():
+    f = np.zeros(256, dtype=np.uint32)
+    f[9] = 1 << 12
+    sym = np.full(100000, 9, dtype=np.uint8)
+    c = R.recoil_encode(sym, f, 12, 8)
+    _check_full(c, sym)
+
+
+@pytest.mark.parametrize("P", [1, 7, 64, 2176])
+def test_partitioned_kernel_vs_oracle(P):
+    sym = synth.text_bytes(1_000_000, 40 + P)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_partitioned_encode(sym, f, 11, P)
+    assert c.tobytes() == oracle.partitioned_encode(sym, f, 11, P)
+    _check_full(c, sym)
+
+
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_sharded_task_ranges(shards):
+    """Multi-GPU data path on one GPU: each shard's plan uploads only its word slice
+    and writes only its output span; the spans tile [0, N) and match the input."""
+    sym = synth.image_bytes(3_000_000, 77)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    for c in (R.recoil_encode(sym, f, 11, 800), R.recoil_partitioned_encode(sym, f, 11, 800)):
+        bounds = R.recoil_shard_plan(c, shards)
+        got = np.zeros(len(sym), dtype=np.uint8)
+        covered = 0
+        for a, b in zip(bounds, bounds[1:]):
+            rc, bad, out, plan = gpu_decode(c, a, b)
+            assert rc == 0, (R.ERRORS.get(rc), bad)
+            assert plan["word_count"] < R.recoil_inspect(c)["n_words"] + 256
+            got[plan["out_lo"]:plan["out_hi"]] = out
+            covered += plan["out_hi"] - plan["out_lo"]
+        assert covered == len(sym) and (got == sym).all()
+
+
+def test_combined_containers_decode_identically():
+    sym = synth.exp_bytes(4_000_000, 50, 88)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 4096)
+    for target in (2048, 256, 16, 1):
+        cc = R.recoil_combine_splits(c, target)
+        assert cc.tobytes() == oracle.combine(c.tobytes(), target)
+        _check_full(cc, sym)
+
+
+def test_corrupted_anchor_is_flagged_or_wrong():
+    """a bit-flipped anchor state desynchronises its task -- the device end-state
+    check (task 0) or the output comparison catches it."""
+    sym = synth.exp_bytes(200000, 50, 5)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 4)
+    info = R.recoil_inspect(c)
+    # first split record's first anchor state sits right after header + finals + global block
+    pos = info["header_bytes"] + 4 * 32
+    # global block size: recompute via oracle parse of an M=1 combine is awkward; brute force
+    # flip each candidate byte of the first record until the container still parses
+    for delta in range(0, 64):
+        bad = c.copy()
+        bad[pos + delta] ^= 0x04
+        try:
+            R.recoil_inspect(bad)
+        except R.RecoilError:
+            continue
+        rc, badt, out, _ = gpu_decode(bad)
+        if rc != 0 or not (out == sym).all():
+            return
+    pytest.fail("no corruption detected")
+
+
+# ------------------------------------------------------------------------------
+# BASELINE.json configs at full size, in the launch configuration bench.py uses
+# ------------------------------------------------------------------------------
+
+def _sampled_oracle_tasks(c, out, k=24):
+    M = R.recoil_inspect(c)["n_splits"]
+    tasks = sorted(set([0, 1, M // 2, M - 2, M - 1] + list(np.linspace(0, M - 1, k).astype(int))))
+    for t in tasks:
+        if 0 <= t < M:
+            want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t))
+            assert (out[lo:hi + 1] == want[lo:hi + 1]).all(), t
+
+
+def test_config1_1MiB_exp50_16_splits():
+    sym = synth.exp_bytes(1 << 20, 50, synth.seed_for(1, 50))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 16)
+    assert c.tobytes() == oracle.recoil_encode(sym, f, 11, 16)
+    _check_full(c, sym)
+
+
+def test_config2_100MiB_text_occupancy_splits():
+    warps, sms = R.recoil_decode_occupancy(0, 11)
+    M = warps * sms * 3
+    sym = synth.text_bytes(100 << 20, synth.seed_for(2))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, M)
+    assert R.recoil_inspect(c)["n_splits"] == M
+    rc, bad, out, _ = gpu_decode(c)
+    assert rc == 0 and (out == sym).all()
+    _sampled_oracle_tasks(c, out)
+    p = R.recoil_partitioned_encode(sym, f, 11, M)
+    rc, bad, out, _ = gpu_decode(p)
+    assert rc == 0 and (out == sym).all()
+
+
+@pytest.mark.parametrize("lam", [10, 50, 100, 200])
+def test_config3_1GiB_exp(lam):
+    warps, sms = R.recoil_decode_occupancy(0, 11)
+    sym = synth.exp_bytes(1 << 30, lam, synth.seed_for(3, lam))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, warps * sms * 8)
+    rc, bad, out, _ = gpu_decode(c)
+    assert rc == 0 and (out == sym).all()
+    _sampled_oracle_tasks(c, out, 8)
+
+
+def test_config4_combine_65536_to_2048_256_16():
+    sym = synth.exp_bytes(1 << 30, 50, synth.seed_for(4, 50))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 65536)
+    assert R.recoil_inspect(c)["n_splits"] == 65536
+    for target in (65536, 2048, 256, 16):
+        cc = R.recoil_combine_splits(c, target)
+        assert R.recoil_inspect(cc)["n_splits"] == target
+        rc, bad, out, _ = gpu_decode(cc)
+        assert rc == 0 and (out == sym).all(), target
+    small = R.recoil_combine_splits(c, 16)
+    assert small.tobytes() == oracle.combine(c.tobytes(), 16)
+    assert (R.recoil_decode_cpu(small) == sym).all()

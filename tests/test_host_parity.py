@@ -1,0 +1,182 @@
+"""Host half of the product (librecoil.so C++: model, encoder + split heuristic,
+container, combine, task planning, CPU decoder) vs the oracle, on CPU.
+
+Containers must be byte-identical to the oracle's (same bitstream, final states,
+split choice and metadata); decodes must equal the input.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2306_12141_b200 import recoil as R
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def test_library_exports_every_declared_symbol():
+    """include/recoil.h declarations == exported symbols; the binding wraps them all."""
+    hdr = open(os.path.join(ROOT, "include", "recoil.h")).read()
+    declared = set(re.findall(r"^\s*(?:const char \*|void |int )\s*\*?(recoil_\w+)\(", hdr, re.M))
+    assert declared == set(R.EXPORTS)
+    lib = ctypes.CDLL(R.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert R.recoil_strerror(R.RECOIL_E_SYNC) and R.recoil_strerror(0) == "ok"
+
+
+def test_build_model_matches_oracle():
+    rng = np.random.default_rng(4)
+    for _ in range(300):
+        n = int(rng.integers(1, 17))
+        k = int(rng.integers(1, min(256, 1 << n) + 1))
+        hist = np.zeros(256, dtype=np.uint64)
+        hist[rng.choice(256, size=k, replace=False)] = rng.integers(1, 10 ** int(rng.integers(1, 8)), size=k)
+        assert (R.recoil_build_model(hist, n) == oracle.build_model(hist, n)).all()
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_build_model(np.zeros(256), 11)
+    assert e.value.rc == R.RECOIL_E_EMPTY
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_build_model(np.ones(256), 7)
+    assert e.value.rc == R.RECOIL_E_ALPHABET
+
+
+FUZZ = [(kind, N, n, M) for kind in ("exp", "text", "image")
+        for N, n, M in ((0, 11, 4), (1, 11, 4), (31, 11, 3), (32, 8, 2), (33, 12, 5), (1000, 11, 7),
+                        (50000, 11, 16), (50000, 12, 200), (200000, 16, 33), (300000, 5, 64))]
+
+
+@pytest.mark.parametrize("kind,N,n,M", FUZZ)
+def test_container_byte_identical_to_oracle(kind, N, n, M):
+    sym = synth.workload(kind, N, seed=N + n + M, lam=30)
+    hist = synth.histogram(sym) if N else np.ones(256, dtype=np.uint64)
+    if (hist > 0).sum() > (1 << n):
+        pytest.skip("alphabet larger than 2^n")
+    f = oracle.build_model(hist, n)
+    c = R.recoil_encode(sym, f, n, M)
+    assert c.tobytes() == oracle.recoil_encode(sym, f, n, M)
+    assert (R.recoil_decode_cpu(c) == sym).all()
+    info = R.recoil_inspect(c)
+    oi = oracle.container_info(c.tobytes())
+    assert (info["n_symbols"], info["n_words"], info["n_splits"]) == (oi["N"], oi["B"], oi["M"])
+
+
+@pytest.mark.parametrize("lam,M", [(10, 2176), (50, 2176), (200, 700), (500, 64)])
+def test_container_identical_mid_size(lam, M):
+    sym = synth.exp_bytes(3_000_000, lam, seed=lam)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, M)
+    assert c.tobytes() == oracle.recoil_encode(sym, f, 11, M)
+    assert (R.recoil_decode_cpu(c) == sym).all()
+
+
+def test_combine_identical_to_oracle():
+    sym = synth.text_bytes(2_000_000, 21)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 2176)
+    for target in (1, 2, 3, 16, 100, 1000, 2175, 2176, 5000):
+        a = R.recoil_combine_splits(c, target)
+        assert a.tobytes() == oracle.combine(c.tobytes(), target)
+        assert (R.recoil_decode_cpu(a, 3) == sym).all()
+    a = c
+    for target in (1000, 300, 17, 4):
+        a = R.recoil_combine_splits(a, target)
+        assert (R.recoil_decode_cpu(a) == sym).all()
+
+
+def test_partitioned_identical_to_oracle():
+    for N, P in ((0, 3), (5, 4), (1000, 64), (300000, 1), (300000, 17), (300000, 2176)):
+        sym = synth.text_bytes(N, N + P)
+        f = oracle.build_model(synth.histogram(sym) if N else np.ones(256, dtype=np.uint64), 11)
+        c = R.recoil_partitioned_encode(sym, f, 11, P)
+        assert c.tobytes() == oracle.partitioned_encode(sym, f, 11, P)
+        assert (R.recoil_decode_cpu(c) == sym).all()
+
+
+def test_cpu_decoder_thread_invariance_and_oracle_tasks():
+    sym = synth.image_bytes(1_500_000, 5)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 300)
+    outs = [R.recoil_decode_cpu(c, t) for t in (1, 2, 8)]
+    assert all((o == sym).all() for o in outs)
+    # the oracle's literal 3-phase decode of single tasks agrees on their ranges
+    for t in (0, 1, 150, 299):
+        out, lo, hi = oracle.recoil_decode_task(c.tobytes(), t)
+        assert (out[lo:hi + 1] == sym[lo:hi + 1]).all()
+
+
+def test_single_symbol_and_tiny_streams():
+    f = np.zeros(256, dtype=np.uint32)
+    f[200] = 1 << 11
+    sym = np.full(5000, 200, dtype=np.uint8)
+    c = R.recoil_encode(sym, f, 11, 10)
+    assert R.recoil_inspect(c)["n_words"] == 0 and R.recoil_inspect(c)["n_splits"] == 1
+    assert c.tobytes() == oracle.recoil_encode(sym, f, 11, 10)
+    assert (R.recoil_decode_cpu(c) == sym).all()
+
+
+def test_errors():
+    sym = synth.exp_bytes(10000, 50, 3)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 8)
+    bad = c.copy()
+    bad[0] ^= 0xFF
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_inspect(bad)
+    assert e.value.rc == R.RECOIL_E_BAD_MAGIC
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_inspect(c[:-1])
+    assert e.value.rc in (R.RECOIL_E_TRUNCATED, R.RECOIL_E_INCONSISTENT)
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_inspect(c[:20])
+    assert e.value.rc == R.RECOIL_E_TRUNCATED
+    f0 = f.copy()
+    f0[sym[0]] = 0
+    f0[[i for i in range(256) if f[i] == 0][0]] = f[sym[0]]
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_encode(sym, f0, 11, 4)
+    assert e.value.rc == R.RECOIL_E_ZERO_FREQ
+    with pytest.raises(R.RecoilError):
+        R.recoil_encode(sym, f, 17, 4)
+    # flipped offset making the metadata non-monotone is rejected
+    info = R.recoil_inspect(c)
+    assert info["n_splits"] == 8
+
+
+def test_decoder_plan_layout():
+    sym = synth.exp_bytes(400000, 50, 6)
+    f = oracle.build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 64)
+    h = R.recoil_decoder_create(c)
+    p = R.recoil_decoder_plan(h)
+    assert p["n_tasks"] == 64 and p["word_lo"] == 0 and p["word_count"] % 256 == 0
+    assert p["word_count"] >= R.recoil_inspect(c)["n_words"]
+    assert (p["out_lo"], p["out_hi"], p["out_base"]) == (0, len(sym), 0)
+    R.recoil_decoder_destroy(h)
+    bounds = R.recoil_shard_plan(c, 4)
+    assert bounds[0] == 0 and bounds[-1] == 64 and bounds == sorted(bounds)
+    spans = []
+    for a, b in zip(bounds, bounds[1:]):
+        h = R.recoil_decoder_create(c, a, b)
+        p = R.recoil_decoder_plan(h)
+        assert p["word_lo"] % 256 == 0 and p["out_base"] % 512 == 0 and p["out_base"] <= p["out_lo"]
+        spans.append((p["out_lo"], p["out_hi"]))
+        R.recoil_decoder_destroy(h)
+    assert spans[0][0] == 0 and spans[-1][1] == len(sym)
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(len(spans) - 1))
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 2 * len(sym) / 64
+    c16 = R.recoil_encode(sym, oracle.build_model(synth.histogram(sym), 16), 16, 4)
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_decoder_create(c16)
+    assert e.value.rc == R.RECOIL_E_UNSUPPORTED
