@@ -79,6 +79,7 @@ def _load():
         "or_container_points": (i32, [P, u64, P, P, P, P]),
         "or_recoil_decode": (i32, [P, u64, P]),
         "or_recoil_decode_task": (i32, [P, u64, u32, P, P, P]),
+        "or_recoil_decode_tasks": (i32, [P, u64, P, u32, P, P]),
         "or_partitioned_encode": (i32, [P, u64, P, u32, u32, u32, P, P]),
         "or_partitioned_decode": (i32, [P, u64, P]),
     }
@@ -279,6 +280,18 @@ def recoil_decode_task(container: bytes, task: int, out: np.ndarray | None = Non
     _check(_load().or_recoil_decode_task(c.ctypes.data, c.size, task, out.ctypes.data, ctypes.byref(lo),
                                          ctypes.byref(hi)))
     return out, lo.value, hi.value
+
+
+def recoil_decode_tasks(container: bytes, tasks, out: np.ndarray | None = None):
+    """Decode a list of tasks with one container parse; returns (out, committed symbols)."""
+    c = _u8(container)
+    N = container_info(container)["N"]
+    if out is None:
+        out = np.zeros(max(N, 1), dtype=np.uint8)
+    t = np.ascontiguousarray(np.asarray(tasks, dtype=np.uint32))
+    n = ctypes.c_uint64(0)
+    _check(_load().or_recoil_decode_tasks(c.ctypes.data, c.size, _ptr(t), t.size, out.ctypes.data, ctypes.byref(n)))
+    return out, n.value
 
 
 def partitioned_encode(sym, f, n: int, P: int, W: int = 32) -> bytes:

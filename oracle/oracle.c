@@ -794,6 +794,27 @@ int or_recoil_decode(const uint8_t *c, uint64_t len, uint8_t *out) {
   return rc;
 }
 
+/* Decode a list of tasks with one parse of the container (bounded samples for
+ * the CPU baseline).  *n_symbols = committed symbols decoded. */
+int or_recoil_decode_tasks(const uint8_t *c, uint64_t len, const uint32_t *tasks, uint32_t n_tasks,
+                           uint8_t *out, uint64_t *n_symbols) {
+  or_box bx;
+  int rc = box_read(c, len, &bx);
+  if (rc) return rc;
+  uint16_t *w = box_words(&bx);
+  uint64_t total = 0;
+  for (uint32_t k = 0; k < n_tasks && rc == OR_OK; ++k) {
+    uint64_t lo = 0, hi = 0;
+    if (tasks[k] >= bx.M || bx.N == 0) { rc = OR_E_ARG; break; }
+    rc = box_task(&bx, w, tasks[k], out, &lo, &hi);
+    total += hi - lo + 1;
+  }
+  if (n_symbols) *n_symbols = total;
+  free(w);
+  box_free(&bx);
+  return rc;
+}
+
 int or_recoil_decode_task(const uint8_t *c, uint64_t len, uint32_t task, uint8_t *out,
                           uint64_t *lo, uint64_t *hi) {
   or_box bx;

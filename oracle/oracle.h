@@ -88,6 +88,8 @@ int or_container_points(const uint8_t *c, uint64_t len, uint64_t *offset, uint64
 int or_recoil_decode(const uint8_t *c, uint64_t len, uint8_t *out);
 int or_recoil_decode_task(const uint8_t *c, uint64_t len, uint32_t task, uint8_t *out,
                           uint64_t *lo, uint64_t *hi);
+int or_recoil_decode_tasks(const uint8_t *c, uint64_t len, const uint32_t *tasks, uint32_t n_tasks,
+                           uint8_t *out, uint64_t *n_symbols);
 
 /* Conventional partitioned codec. */
 int or_partitioned_encode(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
