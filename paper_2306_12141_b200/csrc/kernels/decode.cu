@@ -38,7 +38,7 @@ namespace dev {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
-constexpr int kMinBlocksPerSM = 5;  // 40 resident warps/SM (<= 48 registers)
+constexpr int kMinBlocksPerSM = 5;  // 40 resident warps/SM (<= 48 registers); 48 warps measured slower
 constexpr int kRingChunks = 4;
 constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
 constexpr uint32_t kRingBytes = 2 * kRingWords;
@@ -60,12 +60,17 @@ struct Params {
   uint32_t k4096;         // 2^12: bias = (e * 2^12) >> 20 as IMAD + SHF instead of SHF + LOP3
 };
 
-// Dynamic shared memory: [pad to 2 KB][rings 8 x 2 KB][stages 8 x 512 B][records 8 x 2 x 176 B][LUT 2^n x 4 B]
-constexpr uint32_t kStageOff = kWarpsPerBlock * kRingBytes;
-constexpr uint32_t kRecOff = kStageOff + kWarpsPerBlock * kBlockBytes;
-constexpr uint32_t kLutOff = kRecOff + kWarpsPerBlock * 2 * sizeof(TaskRec);
-static_assert(kLutOff % 16 == 0, "LUT alignment");
-constexpr uint32_t kPadBytes = 2048;
+// Static shared memory per block (about 33 KB for n = 11): the word rings need
+// 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
+template <int NB>
+struct __align__(16) Smem {
+  // 8 x 2 KB word windows + 2 KB so the first can start 2 KB-aligned: the
+  // shared window does not honour more than 1 KB alignment of static data
+  uint16_t ring[kWarpsPerBlock + 1][kRingWords];
+  uint8_t stage[kWarpsPerBlock][kBlockBytes];  // 8 x 512 B output staging
+  TaskRec rec[kWarpsPerBlock][2];              // current / next task record
+  uint32_t lut[1 << NB];                       // packed LUT: s | bias << 8 | f << 20
+};
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
@@ -107,18 +112,15 @@ struct Warp {
   const Params *p;
   uint32_t ring32;   // 2 KB-aligned shared address of this warp's word ring
   uint32_t stage32;  // this warp's 512-B staging block + lane
-  uint32_t lut32;
   uint32_t gt;       // lanes above this one
   int lane;
-  int rot;           // ring rotation: chunk c lives in slot (c + rot) & 3
-  int cursor2;       // 2 x (slice-relative index of the next word to read) + 512 rot
-  int cchunk;        // cursor2 >> 9 at the last window check (rotated chunk index)
+  int cursor2;       // 2 x (slice-relative index of the next word to read)
+  int cchunk;        // cursor2 >> 9 at the last window check
 
-  // a7: warp-cooperative prefetch of rotated chunk cr (256 words = 32 lanes x 16 B)
-  __device__ __forceinline__ void issue_chunk(int cr) {
-    const int c = cr - rot;
+  // a7: warp-cooperative prefetch of word chunk c (256 words = 32 lanes x 16 B)
+  __device__ __forceinline__ void issue_chunk(int c) {
     if (c >= 0 && c < p->n_chunks)
-      cp_async16(ring32 + (uint32_t)(cr & (kRingChunks - 1)) * (2 * kChunkWords) + 16 * lane,
+      cp_async16(ring32 + (uint32_t)(c & (kRingChunks - 1)) * (2 * kChunkWords) + 16 * lane,
                  p->words + (size_t)c * kChunkWords + lane * 8);
     cp_commit();
   }
@@ -146,17 +148,17 @@ struct Warp {
   }
   // Eq. 2 with the packed LUT; stages the symbol byte of group slot k (= g mod 16)
   template <int NB>
-  __device__ __forceinline__ uint32_t decode(uint32_t x, uint32_t k) {
-    const uint32_t e = lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
+  __device__ __forceinline__ uint32_t decode(const uint32_t *lut, uint32_t x, uint32_t k) {
+    const uint32_t e = lut[x & ((1u << NB) - 1)];
     sts_u8(stage32 + k * 32, e);
     return (e >> 20) * (x >> NB) + ((e * p->k4096) >> 20);  // f (x >> n) + bias
   }
-  // a8: write output block b: every 16-B chunk inside [wlo, whi) as one store
-  __device__ __forceinline__ void flush(int b, uint64_t wlo, uint64_t whi) {
+  // a8: write an output block: every 16-B chunk of this lane inside the task's
+  // write window [woff, wend) (offsets relative to the block's base `dst`).
+  __device__ __forceinline__ void flush(uint8_t *dst, int rel, int woff, int wend) {
     __syncwarp();
-    const uint64_t c0 = (uint64_t)(uint32_t)b * kBlockBytes + 16 * lane;
-    if (c0 >= wlo && c0 + 16 <= whi) stg_v4(p->out + (c0 - p->out_base), lds_v4(stage32 + 15 * lane));
-    __syncwarp();
+    const int c = rel + 16 * lane;
+    if (c >= woff && c + 16 <= wend) stg_v4(dst + 16 * lane, lds_v4(stage32 + 15 * lane));
   }
 };
 
@@ -164,22 +166,23 @@ struct Warp {
 // initialised with its anchor state in its anchor group, before its read;
 // uninitialised lanes keep x = 0xFFFFFFFF and their decodes are discarded.
 template <int NB, bool SYNC>
-__device__ __forceinline__ uint32_t step(Warp &w, uint32_t x, int g, int k, int init_group, uint32_t state) {
+__device__ __forceinline__ uint32_t step(Warp &w, const uint32_t *lut, uint32_t x, int g, int k, int init_group,
+                                         uint32_t state) {
   if (SYNC && g == init_group) x = state;
   x = w.refill(x);
-  const uint32_t xn = w.decode<NB>(x, (uint32_t)k);
+  const uint32_t xn = w.decode<NB>(lut, x, (uint32_t)k);
   return (SYNC && g > init_group) ? 0xFFFFFFFFu : xn;
 }
 
 // Groups g .. g_end of one 16-group output block (g_end <= g, same block),
 // entered at slot g & 15 (Duff's device) and left after slot g_end & 15.
 template <int NB, bool SYNC>
-__device__ __forceinline__ uint32_t run_part(Warp &w, uint32_t x, int g, int g_end, int init_group,
-                                             uint32_t state) {
+__device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, uint32_t x, int g, int g_end,
+                                             int init_group, uint32_t state) {
   const int gb = g & ~15, k1 = g_end & 15;
   w.window_check();
 #define RECOIL_STEP(K)                                                  \
-  x = step<NB, SYNC>(w, x, gb + K, K, init_group, state);               \
+  x = step<NB, SYNC>(w, lut, x, gb + K, K, init_group, state);          \
   if (k1 == K) break;
   switch (g & 15) {
     case 15: RECOIL_STEP(15) [[fallthrough]];
@@ -208,63 +211,54 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, uint32_t x, int g, int g_e
 
 // A whole 16-group block with every lane initialised: no branch per group.
 template <int NB>
-__device__ __forceinline__ uint32_t run_block(Warp &w, uint32_t x) {
+__device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, uint32_t x) {
   w.window_check();
 #pragma unroll
   for (int k = 15; k >= 8; --k) {
     x = w.refill(x);
-    x = w.decode<NB>(x, k);
+    x = w.decode<NB>(lut, x, k);
   }
   w.window_check();
 #pragma unroll
   for (int k = 7; k >= 0; --k) {
     x = w.refill(x);
-    x = w.decode<NB>(x, k);
+    x = w.decode<NB>(lut, x, k);
   }
   return x;
 }
 
 template <int NB>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kernel(const Params p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // the dynamic window starts 1 KB-aligned; the rings need 2 KB alignment
-  const uint32_t base32 = (smem_addr(smem_raw) + kPadBytes - 1) & ~(kPadBytes - 1);
-  unsigned char *const smem = smem_raw + (base32 - smem_addr(smem_raw));
-  const uint32_t lut_words = 1u << NB;
+  __shared__ Smem<NB> sm;
 
   // a2: stage the packed LUT in shared memory (per block)
-  {
-    unsigned char *lut_g = smem + kLutOff;
-    if (NB >= 2) {
-      for (uint32_t i = threadIdx.x; i < lut_words / 4; i += kThreads)
-        reinterpret_cast<int4 *>(lut_g)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
-    } else if (threadIdx.x < lut_words) {
-      reinterpret_cast<uint32_t *>(lut_g)[threadIdx.x] = p.lut[threadIdx.x];
-    }
+  if (NB >= 2) {
+    for (uint32_t i = threadIdx.x; i < (1u << NB) / 4; i += kThreads)
+      reinterpret_cast<int4 *>(sm.lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+  } else if (threadIdx.x < (1u << NB)) {
+    sm.lut[threadIdx.x] = p.lut[threadIdx.x];
   }
   __syncthreads();
 
   Warp w;
   w.p = &p;
   w.lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  w.ring32 = base32 + warp * kRingBytes;
-  w.stage32 = base32 + kStageOff + warp * kBlockBytes + w.lane;
-  w.lut32 = base32 + kLutOff;
-  w.gt = lanemask_gt();
-  w.rot = 0;
-  w.cchunk = 2;  // first task: any stale slot
-  const uint32_t rec32 = base32 + kRecOff + warp * 2 * sizeof(TaskRec);
-  const unsigned char *rec_g = smem + kRecOff + warp * 2 * sizeof(TaskRec);
   const int lane = w.lane;
+  const int warp = threadIdx.x >> 5;
+  w.ring32 = ((smem_addr(&sm.ring[0][0]) + kRingBytes - 1) & ~(kRingBytes - 1)) + warp * kRingBytes;
+  w.stage32 = smem_addr(&sm.stage[warp][lane]);
+  w.gt = lanemask_gt();
+  w.cchunk = 0;
+  const uint32_t rec32 = smem_addr(&sm.rec[warp][0]);
+  const uint32_t *lut = sm.lut;
 
   // a3: persistent warps.  The first wave of task ids is static; afterwards a
   // warp takes the next id from an atomic counter shortly before it finishes
   // its current task (two blocks ahead: the atomic's latency hides behind them)
   // and streams that record into shared memory by cp.async.  Taking ids late
-  // matters: warps of one SM run at very different speeds under the
-  // oldest/highest-priority issue policy, so an id reserved early by a slow
-  // warp would become the kernel's tail.
+  // matters: warps of one SM run at very different speeds under the issue
+  // arbiter's priority order, so an id reserved early by a slow warp would
+  // become the kernel's tail.
   const uint32_t first_wave = gridDim.x * kWarpsPerBlock;
   auto issue_task = [&](uint32_t t, int buf) {
     if (t < p.n_tasks && lane < (int)(sizeof(TaskRec) / 16))
@@ -276,9 +270,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
   int buf = 0;
   if (t < p.n_tasks) issue_task(t, 0);
   while (t < p.n_tasks) {
-    cp_wait<0>();  // this task's record (and any stale window copy) has landed
+    cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
-    const TaskRec &r = *reinterpret_cast<const TaskRec *>(rec_g + buf * sizeof(TaskRec));
+    const TaskRec &r = sm.rec[warp][buf];
     const int32_t start_group = r.start_group;
     const uint64_t lo = r.commit_lo, whi = r.write_hi;
     const int64_t end_cursor = r.end_cursor;
@@ -302,13 +296,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
       }
     };
 
-    // a7: word window.  The previous task may have one chunk copy in flight into
-    // slot (cchunk - 2) & 3; rotate so that slot is this task's 4th chunk, which
-    // is only issued after the first wait below has retired the stale copy.
-    const int stale_slot = (w.cchunk - 2) & 3;
-    w.rot = (stale_slot - (cursor0 >> 8) + 3) & 3;
-    w.cursor2 = 2 * cursor0 + 512 * w.rot;
-    w.cchunk = w.cursor2 >> 9;
+    // a7: word window -- chunks c, c-1 resident, c-2 in flight
+    w.cursor2 = 2 * cursor0;
+    w.cchunk = cursor0 >> 8;
     w.issue_chunk(w.cchunk);
     w.issue_chunk(w.cchunk - 1);
     w.issue_chunk(w.cchunk - 2);
@@ -316,11 +306,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
     __syncwarp();
 
     const int32_t lo_group = (int32_t)(lo >> 5);
-    const uint64_t wlo = (uint64_t)lo_group * kLanes;
     int32_t min_init = init_group;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) min_init = min(min_init, __shfl_xor_sync(kFull, min_init, o));
     const int32_t g_sync_end = max(min_init, lo_group);
+    // 32-bit output bookkeeping relative to the block of lo_group
+    const int32_t b_lo = lo_group >> 4;
+    uint8_t *const out_blo = p.out + ((uint64_t)b_lo * kBlockBytes - p.out_base);
+    const int woff = lo_group * (int)kLanes - b_lo * (int)kBlockBytes;  // 0..511
+    const int wend = (int)(whi - (uint64_t)b_lo * kBlockBytes);
 
     uint32_t x = 0xFFFFFFFFu;  // uninitialised: never < L
     int32_t g = start_group;
@@ -328,27 +322,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
     // a4: Synchronization Phase -- groups where some lane is still uninitialised
     while (g >= g_sync_end) {
       const int gb = g & ~15, ge = max(gb, g_sync_end);
-      x = run_part<NB, true>(w, x, g, ge, init_group, state);
-      if (ge == gb) w.flush(gb >> 4, wlo, whi);
+      x = run_part<NB, true>(w, lut, x, g, ge, init_group, state);
+      if (ge == gb) {
+        const int rel = (gb >> 4) - b_lo;
+        w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
+      }
       g = ge - 1;
     }
     // a5 + a6: Decoding Phase and Cross-Boundary Phase (all lanes initialised)
-    while (g >= lo_group) {
+    if (g >= lo_group && (g & 15) != 15) {  // head: partial block
       const int gb = g & ~15, ge = max(gb, lo_group);
-      if ((g & 15) == 15 && ge == gb)
-        x = run_block<NB>(w, x);
-      else
-        x = run_part<NB, false>(w, x, g, ge, 0, 0);
-      w.flush(gb >> 4, wlo, whi);
+      x = run_part<NB, false>(w, lut, x, g, ge, 0, 0);
+      const int rel = (gb >> 4) - b_lo;
+      w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
       g = ge - 1;
-      if (g - lo_group < 48) next_task_step();
+    }
+    if (g >= lo_group) {
+      // whole blocks above the block of lo_group; the next task id is requested
+      // two blocks before the end
+      int rel = (g >> 4) - b_lo;
+      const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
+      for (; rel >= full_lo; --rel) {
+        if (rel - full_lo < 3) next_task_step();
+        x = run_block<NB>(w, lut, x);
+        w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
+      }
+      if (full_lo) {  // tail: the partial block of lo_group
+        x = run_part<NB, false>(w, lut, x, b_lo * 16 + 15, lo_group, 0, 0);
+        w.flush(out_blo, 0, woff, wend);
+      }
     }
     while (next_state < 2) next_task_step();
 
     // a9: integrity -- a task that reaches its codec's start must end in the
     // stack-property end state: cursor one below the codec's first word,
     // every initialised lane back at L.
-    const int cursor = (w.cursor2 - 512 * w.rot) >> 1;
+    const int cursor = w.cursor2 >> 1;
     bool bad_end = false;
     const bool under = cursor < -1;
     if (end_cursor != kNoEndCheck) {
@@ -386,7 +395,7 @@ static KernelFn kernel_for(uint32_t nbits) {
 
 }  // namespace dev
 
-static size_t smem_bytes(uint32_t nbits) { return dev::kPadBytes + dev::kLutOff + ((size_t)4 << nbits); }
+static size_t smem_bytes(uint32_t nbits) { return 0; }  // static shared memory only
 
 static int configure(dev::KernelFn fn, uint32_t nbits) {
   cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
