@@ -41,6 +41,8 @@ CONFIGS = {
     "config2": ("text", 100 << 20, 0.0, "100 MiB text-like (Zipf-96, ~5.09 bit/B) bytes, n=11, "
                                          "splits tuned to the kernel's resident warps"),
     "config3": ("exp", 1 << 30, 50.0, "1 GiB exponential (lambda=50) bytes, n=11, occupancy-tuned splits"),
+    "config4": ("exp", 1 << 30, 50.0, "1 GiB exponential (lambda=50) bytes, n=11, one encode with 65536 splits "
+                                      "combined (P:266-272) to --combine-to splits"),
     "config5": ("image", 1 << 30, 0.0, "image-residual-like bytes (Laplace mixture, ~2.3 bit/B), n=11, "
                                        "sharded by split range (1 GiB per GPU)"),
 }
@@ -117,9 +119,10 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_stream(cfg: str, world: int, prob_bits: int = 11):
+def make_stream(cfg: str, world: int, lam_override: float = 0.0):
     import synth
     kind, n, lam, _ = CONFIGS[cfg]
+    lam = lam_override or lam
     n_total = n * world
     sym = synth.workload(kind, n_total, seed=synth.seed_for(int(cfg[-1]), lam), lam=lam or 50.0)
     return sym
@@ -157,7 +160,7 @@ def run_reference(args, rank, world):
         return 0
     import oracle  # noqa: F401
     from paper_2306_12141_b200 import recoil as R
-    sym = make_stream(args.config, world)
+    sym = make_stream(args.config, world, args.lam)
     f = R.recoil_build_model(np.bincount(sym, minlength=256).astype(np.uint64), 11)
     M = args.splits or 11840 * world
     c = R.recoil_encode(sym, f, 11, M)
@@ -193,6 +196,8 @@ def main():
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
     ap.add_argument("--waves", type=int, default=2, help="splits per GPU = waves x resident warps")
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
+    ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
+    ap.add_argument("--lam", type=float, default=0.0, help="config3/4: override lambda")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip partitioned / size-overhead legs")
@@ -208,25 +213,34 @@ def main():
     import __graft_entry__
     if rank == 0 or not os.path.exists(R.LIB_PATH):
         __graft_entry__.build()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
+        # control plane only (barriers, max-over-ranks timing): the decode has no
+        # data-path exchange, so no NCCL collective is on the timed path
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("gloo")
         pg = dist
         dist.barrier()
     R.load()
 
     # ---------------- setup (untimed): synthetic stream, encode, shard plan ----------------
     t_setup = time.perf_counter()
-    sym = make_stream(args.config, world)
+    sym = make_stream(args.config, world, args.lam)
     N_total = len(sym)
     hist = np.bincount(sym, minlength=256).astype(np.uint64)
     f = R.recoil_build_model(hist, 11)
     warps, sms = R.recoil_decode_occupancy(local, 11)
     M_gpu = args.splits or (16 if args.config == "config1" else warps * sms * args.waves)
-    c = R.recoil_encode(sym, f, 11, M_gpu * world)
+    if args.config == "config4":
+        c_full = R.recoil_encode(sym, f, 11, 65536 * world)
+        M_gpu = args.combine_to
+        c = R.recoil_combine_splits(c_full, M_gpu * world)
+        del c_full
+    else:
+        c = R.recoil_encode(sym, f, 11, M_gpu * world)
     info = R.recoil_inspect(c)
     M = info["n_splits"]
     bounds = R.recoil_shard_plan(c, world)
@@ -279,10 +293,10 @@ def main():
         times = timed_decode(dec, args.steps, args.warmup)
     total_ms = float(sum(times))
     if pg:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         total_ms = float(t.item())
-        okt = torch.tensor([1 if ok else 0], device=dev)
+        okt = torch.tensor([1 if ok else 0], dtype=torch.int64)
         pg.all_reduce(okt, op=pg.ReduceOp.MIN)
         ok = bool(okt.item())
     value = N_total * args.steps / (total_ms / 1e3) / 1e9
@@ -313,7 +327,7 @@ def main():
             e2e_times.append(dt)
     e2e_s = float(np.mean(e2e_times))
     if pg:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = N_total / e2e_s / 1e9
@@ -384,8 +398,11 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": args.config + ": " + CONFIGS[args.config][3], "n_symbols": int(N_total),
                        "n_symbols_per_gpu": int(CONFIGS[args.config][1]), "splits": int(M),
-                       "splits_rule": f"{args.waves} waves x {warps} resident warps/SM x {sms} SMs per GPU"
-                       if not args.splits and args.config != "config1" else "fixed",
+                       "splits_rule": (f"65536 x {world} encoded, combined to {M_gpu} x {world}"
+                                       if args.config == "config4" else
+                                       f"{args.waves} waves x {warps} resident warps/SM x {sms} SMs per GPU"
+                                       if not args.splits and args.config != "config1" else "fixed"),
+                       "lambda": (args.lam or CONFIGS[args.config][2]) if CONFIGS[args.config][0] == "exp" else None,
                        "compressed_bytes": int(len(c)), "prob_bits": 11, "lanes": 32,
                        "parallelism": f"split-range shards x{world}",
                        "l2": "flushed before every timed step (256 MiB write, outside the events)"},
