@@ -136,6 +136,12 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
     p.out_lo = d->tasks.front().commit_lo;
     p.out_hi = d->tasks.back().commit_hi + 1;
   }
+  // Longest task first: the persistent warps take tasks in table order, so the
+  // kernel's tail is made of the shortest tasks (LPT order).  Output positions
+  // are per task, so the order does not change the result.
+  std::stable_sort(d->tasks.begin(), d->tasks.end(), [](const TaskRec &a, const TaskRec &b) {
+    return a.start_group - (int64_t)(a.commit_lo / kLanes) > b.start_group - (int64_t)(b.commit_lo / kLanes);
+  });
   p.out_base = p.out_lo & ~(uint64_t)(kBlockBytes - 1);
   uint64_t write_end = p.out_hi;
   for (const TaskRec &r : d->tasks) write_end = std::max(write_end, r.write_hi);

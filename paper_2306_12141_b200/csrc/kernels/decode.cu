@@ -38,7 +38,10 @@ namespace dev {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
-constexpr int kMinBlocksPerSM = 5;  // 40 resident warps/SM (<= 48 registers); 48 warps measured slower
+#ifndef RECOIL_MIN_BLOCKS
+#define RECOIL_MIN_BLOCKS 5
+#endif
+constexpr int kMinBlocksPerSM = RECOIL_MIN_BLOCKS;  // 5: 40 resident warps/SM (<= 48 registers); 48 warps measured slower
 constexpr int kRingChunks = 4;
 constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
 constexpr uint32_t kRingBytes = 2 * kRingWords;

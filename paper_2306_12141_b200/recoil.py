@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librecoil.so")
+LIB_PATH = os.environ.get("RECOIL_LIB") or os.path.join(_PKG, "librecoil.so")  # RECOIL_LIB: experiment builds
 _lib = None
 
 RECOIL_OK = 0
