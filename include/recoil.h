@@ -9,7 +9,9 @@
  *
  * Fixed parameters (tab:rans_params P:400-423): 32-bit states, L = 2^16,
  * b = 16-bit words, 8-bit symbols, W = 32 lanes, 1 <= n <= 16 probability
- * bits for encoding; the GPU decoder supports n <= 12 (packed LUT).
+ * bits.  The GPU decoder packs s, f, F into one u32 LUT entry for n <= 12
+ * and uses a slot -> symbol byte table plus a per-symbol (f, F)
+ * table for 13 <= n <= 16.
  * Symbol i (0-based) belongs to lane i mod 32 and group i / 32.
  *
  * Conventions for every call:
@@ -50,7 +52,7 @@ extern "C" {
 #define RECOIL_E_CUDA (-12)        /* a CUDA runtime call failed                  */
 #define RECOIL_E_NOMEM (-13)       /* host allocation failed                      */
 #define RECOIL_E_BUFFER (-14)      /* output buffer too small (*len = required)   */
-#define RECOIL_E_UNSUPPORTED (-15) /* valid but outside the GPU path (n > 12)     */
+#define RECOIL_E_UNSUPPORTED (-15) /* valid but outside the GPU path (slice >= 2^31 words) */
 
 const char *recoil_strerror(int status);
 
@@ -141,7 +143,8 @@ typedef struct {
  * enters at split point t+1; task M-1 enters from the final
  * states.  Works on either container kind (partitions = tasks).
  * The container bytes must stay valid while the handle is used.
- * Errors: container errors, E_ARG, E_NOMEM, E_UNSUPPORTED (n > 12). */
+ * Errors: container errors, E_ARG, E_NOMEM, E_UNSUPPORTED (word slice of
+ * 2^31 words or more). */
 int recoil_decoder_create(const uint8_t *container, uint64_t len, uint64_t task_begin,
                           uint64_t task_end, recoil_decoder **out);
 int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan);
@@ -176,7 +179,7 @@ void recoil_decoder_destroy(recoil_decoder *dec);
 /* Resident warps per SM of the decode kernel on `device` and the SM count
  * (cudaOccupancyMaxActiveBlocksPerMultiprocessor): the split count
  * that fills the GPU is warps_per_sm * sm_count * waves. */
-int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);
+int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);  /* 1 <= n <= 16 */
 
 /* ---------------------------------------------------------------------- */
 /* Multi-GPU sharding (host planning; each GPU decodes its own task range) */

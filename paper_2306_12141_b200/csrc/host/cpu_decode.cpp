@@ -53,6 +53,12 @@ int decode_task(const Decoder &d, const Tables &tb, const TaskRec &t, const uint
     }
   }
   if (t.end_cursor != kNoEndCheck) {
+    // reached the codec's first symbol: outputs emitted before group 0 (n = 16, f = 1)
+    for (int32_t j = kLanes - 1; j >= 0; --j)
+      if (inited[j] && x[j] < kL) {
+        if (cur < 0) return RECOIL_E_UNDERFLOW;
+        x[j] = (x[j] << kWordBits) | w[cur--];
+      }
     if (cur != t.end_cursor) return RECOIL_E_SYNC;
     for (uint32_t j = 0; j < kLanes; ++j)
       if (inited[j] && x[j] != kL) return RECOIL_E_SYNC;

@@ -18,13 +18,27 @@
 
 namespace recoil {
 
-void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint32_t> *lut) {
-  lut->assign((size_t)1 << n, 0);
-  uint32_t F = 0;
+void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut) {
+  if (n <= 12) {  // packed: s | bias << 8 | f << 20 (symbol, f and F in one 32-bit entry)
+    std::vector<uint32_t> w((size_t)1 << n, 0);
+    uint32_t F = 0;
+    for (uint32_t s = 0; s < 256; ++s) {
+      for (uint32_t k = 0; k < f[s]; ++k) w[F + k] = s | (k << 8) | (f[s] << 20);
+      F += f[s];
+    }
+    lut->resize(4 * w.size());
+    std::memcpy(lut->data(), w.data(), lut->size());
+    return;
+  }
+  // n = 13..16: slot -> symbol bytes, then per symbol f | F << 16
+  lut->assign(((size_t)1 << n) + 1024, 0);
+  uint32_t F = 0, fF[256];
   for (uint32_t s = 0; s < 256; ++s) {
-    for (uint32_t k = 0; k < f[s]; ++k) (*lut)[F + k] = s | (k << 8) | (f[s] << 20);  // s | bias | f
+    std::memset(lut->data() + F, (int)s, f[s]);
+    fF[s] = (f[s] & 0xFFFFu) | (F << 16);
     F += f[s];
   }
+  std::memcpy(lut->data() + ((size_t)1 << n), fF, 1024);
 }
 
 static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
@@ -44,7 +58,7 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
       d->single_symbol = s;
     }
   if (present != 1) d->single_symbol = -1;
-  if (c.n <= kMaxGpuProbBits) pack_lut(c.f, c.n, &d->lut);
+  if (for_gpu) pack_lut(c.f, c.n, &d->lut);
   d->tasks.clear();
   d->finals.clear();
   std::vector<uint64_t> part_start;
@@ -147,7 +161,7 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
   for (const TaskRec &r : d->tasks) write_end = std::max(write_end, r.write_hi);
   p.out_count = ((write_end + 15) & ~15ull) - p.out_base;
   d->lut_off = 16;
-  d->finals_off = align16(d->lut_off + 4 * d->lut.size());
+  d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
   p.workspace_bytes = align16(d->tasks_off + sizeof(TaskRec) * d->tasks.size());
   p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);

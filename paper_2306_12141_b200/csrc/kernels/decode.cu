@@ -48,7 +48,7 @@ constexpr uint32_t kRingBytes = 2 * kRingWords;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 struct Params {
-  const uint32_t *lut;
+  const uint8_t *lut;     // n <= 12: 2^n packed u32; n >= 13: 2^n symbol bytes + 256 x u32 (f | F << 16)
   const uint32_t *finals;
   const TaskRec *tasks;
   DeviceStatus *status;
@@ -65,6 +65,7 @@ struct Params {
 
 // Static shared memory per block (about 33 KB for n = 11): the word rings need
 // 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
+constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 template <int NB>
 struct __align__(16) Smem {
   // 8 x 2 KB word windows + 2 KB so the first can start 2 KB-aligned: the
@@ -72,7 +73,9 @@ struct __align__(16) Smem {
   uint16_t ring[kWarpsPerBlock + 1][kRingWords];
   uint8_t stage[kWarpsPerBlock][kBlockBytes];  // 8 x 512 B output staging
   TaskRec rec[kWarpsPerBlock][2];              // current / next task record
-  uint32_t lut[1 << NB];                       // packed LUT: s | bias << 8 | f << 20
+  // n <= 12: packed LUT s | bias << 8 | f << 20.  n >= 13 (NEXT row 1):
+  // f and F per symbol here, the 2^n slot -> symbol bytes in dynamic smem.
+  uint32_t lut[NB <= kNarrowMaxBits ? (1 << NB) : 256];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -149,12 +152,20 @@ struct Warp {
     cursor2 += total * p->neg2;
     return need ? x * 65536u + w : x;
   }
-  // Eq. 2 with the packed LUT; stages the symbol byte of group slot k (= g mod 16)
+  // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
   template <int NB>
-  __device__ __forceinline__ uint32_t decode(const uint32_t *lut, uint32_t x, uint32_t k) {
-    const uint32_t e = lut[x & ((1u << NB) - 1)];
-    sts_u8(stage32 + k * 32, e);
-    return (e >> 20) * (x >> NB) + ((e * p->k4096) >> 20);  // f (x >> n) + bias
+  __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
+    if constexpr (NB <= kNarrowMaxBits) {
+      const uint32_t e = lut[x & ((1u << NB) - 1)];
+      sts_u8(stage32 + k * 32, e);
+      return (e >> 20) * (x >> NB) + ((e * p->k4096) >> 20);  // f (x >> n) + bias
+    } else {
+      const uint32_t slot = x & ((1u << NB) - 1);
+      const uint32_t s = sym[slot];
+      const uint32_t e = lut[s];  // f | F << 16
+      sts_u8(stage32 + k * 32, s);
+      return (e & 0xFFFFu) * (x >> NB) + slot - (e >> 16);  // f (x >> n) + slot - F
+    }
   }
   // a8: write an output block: every 16-B chunk of this lane inside the task's
   // write window [woff, wend) (offsets relative to the block's base `dst`).
@@ -162,6 +173,7 @@ struct Warp {
     __syncwarp();
     const int c = rel + 16 * lane;
     if (c >= woff && c + 16 <= wend) stg_v4(dst + 16 * lane, lds_v4(stage32 + 15 * lane));
+    __syncwarp();  // the staging block is rewritten by the next group steps
   }
 };
 
@@ -169,23 +181,24 @@ struct Warp {
 // initialised with its anchor state in its anchor group, before its read;
 // uninitialised lanes keep x = 0xFFFFFFFF and their decodes are discarded.
 template <int NB, bool SYNC>
-__device__ __forceinline__ uint32_t step(Warp &w, const uint32_t *lut, uint32_t x, int g, int k, int init_group,
+__device__ __forceinline__ uint32_t step(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x, int g, int k, int init_group,
                                          uint32_t state) {
   if (SYNC && g == init_group) x = state;
   x = w.refill(x);
-  const uint32_t xn = w.decode<NB>(lut, x, (uint32_t)k);
+  const uint32_t xn = w.decode<NB>(lut, sym, x, (uint32_t)k);
   return (SYNC && g > init_group) ? 0xFFFFFFFFu : xn;
 }
 
 // Groups g .. g_end of one 16-group output block (g_end <= g, same block),
 // entered at slot g & 15 (Duff's device) and left after slot g_end & 15.
 template <int NB, bool SYNC>
-__device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, uint32_t x, int g, int g_end,
+__device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x, int g,
+                                             int g_end,
                                              int init_group, uint32_t state) {
   const int gb = g & ~15, k1 = g_end & 15;
   w.window_check();
 #define RECOIL_STEP(K)                                                  \
-  x = step<NB, SYNC>(w, lut, x, gb + K, K, init_group, state);          \
+  x = step<NB, SYNC>(w, lut, sym, x, gb + K, K, init_group, state);     \
   if (k1 == K) break;
   switch (g & 15) {
     case 15: RECOIL_STEP(15) [[fallthrough]];
@@ -214,18 +227,18 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, uint3
 
 // A whole 16-group block with every lane initialised: no branch per group.
 template <int NB>
-__device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, uint32_t x) {
+__device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x) {
   w.window_check();
 #pragma unroll
   for (int k = 15; k >= 8; --k) {
     x = w.refill(x);
-    x = w.decode<NB>(lut, x, k);
+    x = w.decode<NB>(lut, sym, x, k);
   }
   w.window_check();
 #pragma unroll
   for (int k = 7; k >= 0; --k) {
     x = w.refill(x);
-    x = w.decode<NB>(lut, x, k);
+    x = w.decode<NB>(lut, sym, x, k);
   }
   return x;
 }
@@ -233,13 +246,21 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, uint
 template <int NB>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kernel(const Params p) {
   __shared__ Smem<NB> sm;
+  extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
 
-  // a2: stage the packed LUT in shared memory (per block)
-  if (NB >= 2) {
-    for (uint32_t i = threadIdx.x; i < (1u << NB) / 4; i += kThreads)
-      reinterpret_cast<int4 *>(sm.lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
-  } else if (threadIdx.x < (1u << NB)) {
-    sm.lut[threadIdx.x] = p.lut[threadIdx.x];
+  // a2: stage the LUT in shared memory (per block)
+  if constexpr (NB <= kNarrowMaxBits) {
+    constexpr uint32_t kWords = 1u << NB;
+    if (kWords >= 4) {
+      for (uint32_t i = threadIdx.x; i < kWords / 4; i += kThreads)
+        reinterpret_cast<int4 *>(sm.lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+    } else if (threadIdx.x < kWords) {
+      sm.lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut)[threadIdx.x];
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < (1u << NB) / 16; i += kThreads)
+      reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+    sm.lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut + (1u << NB))[threadIdx.x];
   }
   __syncthreads();
 
@@ -254,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
   w.cchunk = 0;
   const uint32_t rec32 = smem_addr(&sm.rec[warp][0]);
   const uint32_t *lut = sm.lut;
+  const uint8_t *sym = sym_dyn;
 
   // a3: persistent warps.  The first wave of task ids is static; afterwards a
   // warp takes the next id from an atomic counter shortly before it finishes
@@ -325,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
     // a4: Synchronization Phase -- groups where some lane is still uninitialised
     while (g >= g_sync_end) {
       const int gb = g & ~15, ge = max(gb, g_sync_end);
-      x = run_part<NB, true>(w, lut, x, g, ge, init_group, state);
+      x = run_part<NB, true>(w, lut, sym, x, g, ge, init_group, state);
       if (ge == gb) {
         const int rel = (gb >> 4) - b_lo;
         w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
     // a5 + a6: Decoding Phase and Cross-Boundary Phase (all lanes initialised)
     if (g >= lo_group && (g & 15) != 15) {  // head: partial block
       const int gb = g & ~15, ge = max(gb, lo_group);
-      x = run_part<NB, false>(w, lut, x, g, ge, 0, 0);
+      x = run_part<NB, false>(w, lut, sym, x, g, ge, 0, 0);
       const int rel = (gb >> 4) - b_lo;
       w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
       g = ge - 1;
@@ -347,15 +369,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
       const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
       for (; rel >= full_lo; --rel) {
         if (rel - full_lo < 3) next_task_step();
-        x = run_block<NB>(w, lut, x);
+        x = run_block<NB>(w, lut, sym, x);
         w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
       }
       if (full_lo) {  // tail: the partial block of lo_group
-        x = run_part<NB, false>(w, lut, x, b_lo * 16 + 15, lo_group, 0, 0);
+        x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
         w.flush(out_blo, 0, woff, wend);
       }
     }
     while (next_state < 2) next_task_step();
+    if (end_cursor != kNoEndCheck) {
+      // the task reached its codec's first symbol: the outputs emitted before
+      // group 0 (Eq. 3 with f(s_0) 2^(32-n) <= L, i.e. n = 16 and f = 1) are read last
+      w.window_check();
+      x = w.refill(x);
+    }
 
     // a9: integrity -- a task that reaches its codec's start must end in the
     // stack-property end state: cursor one below the codec's first word,
@@ -392,13 +420,19 @@ static KernelFn kernel_for(uint32_t nbits) {
     case 10: return recoil_decode_kernel<10>;
     case 11: return recoil_decode_kernel<11>;
     case 12: return recoil_decode_kernel<12>;
+    case 13: return recoil_decode_kernel<13>;
+    case 14: return recoil_decode_kernel<14>;
+    case 15: return recoil_decode_kernel<15>;
+    case 16: return recoil_decode_kernel<16>;
     default: return nullptr;
   }
 }
 
 }  // namespace dev
 
-static size_t smem_bytes(uint32_t nbits) { return 0; }  // static shared memory only
+static size_t smem_bytes(uint32_t nbits) {  // dynamic part only: the slot -> symbol table for n >= 13
+  return nbits > (uint32_t)dev::kNarrowMaxBits ? (size_t)1 << nbits : 0;
+}
 
 static int configure(dev::KernelFn fn, uint32_t nbits) {
   cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -429,8 +463,8 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   char *ws = reinterpret_cast<char *>(d_workspace);
   const recoil_plan &p = d->plan;
   if (cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return RECOIL_E_CUDA;
-  if (!d->lut.empty() && cudaMemcpyAsync(ws + d->lut_off, d->lut.data(), 4 * d->lut.size(),
-                                         cudaMemcpyHostToDevice, s) != cudaSuccess)
+  if (!d->lut.empty() && cudaMemcpyAsync(ws + d->lut_off, d->lut.data(), d->lut.size(), cudaMemcpyHostToDevice,
+                                         s) != cudaSuccess)
     return RECOIL_E_CUDA;
   if (!d->finals.empty() && cudaMemcpyAsync(ws + d->finals_off, d->finals.data(), 4 * d->finals.size(),
                                             cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -473,7 +507,7 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
     if (d->blocks_per_sm < 1) return RECOIL_E_CUDA;
   }
   dev::Params prm;
-  prm.lut = reinterpret_cast<const uint32_t *>(ws + d->lut_off);
+  prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
   prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
   prm.tasks = reinterpret_cast<const TaskRec *>(ws + d->tasks_off);
   prm.status = reinterpret_cast<DeviceStatus *>(ws);

@@ -14,7 +14,7 @@ constexpr uint32_t kL = 1u << 16;        // L
 constexpr uint32_t kWordBits = 16;       // b
 constexpr uint32_t kChunkWords = 256;    // device word-window chunk: 32 lanes x 16 B
 constexpr uint32_t kBlockBytes = 512;    // device output block: 16 groups x 32 symbols
-constexpr uint32_t kMaxGpuProbBits = 12; // packed u32 LUT limit
+constexpr uint32_t kMaxGpuProbBits = 16; // GPU decode: packed u32 LUT up to n = 12, split tables above
 constexpr uint32_t kNoFinals = 0xFFFFFFFFu;
 constexpr int64_t kNoEndCheck = INT64_MIN;
 
@@ -74,7 +74,8 @@ struct DeviceStatus {   // first 16 B of the workspace, zeroed before every deco
 struct Decoder {
   Container c;
   recoil_plan plan{};
-  std::vector<uint32_t> lut;       // 2^n packed entries: s | bias << 8 | f << 20
+  std::vector<uint8_t> lut;        // n <= 12: 2^n packed u32 s | bias << 8 | f << 20;
+                                   // n >= 13: 2^n symbol bytes + 256 x u32 (f | F << 16)
   std::vector<uint32_t> finals;    // K x 32 u32 states referenced by finals_idx
   std::vector<TaskRec> tasks;
   uint64_t lut_off = 0, finals_off = 0, tasks_off = 0;  // workspace byte offsets
@@ -84,7 +85,7 @@ struct Decoder {
 
 int build_decoder(const uint8_t *c, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
                   bool for_gpu);
-void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint32_t> *lut);
+void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
 
 
 }  // namespace recoil

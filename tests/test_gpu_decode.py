@@ -50,7 +50,9 @@ for i, (N, n, M, kind) in enumerate([
         (1, 11, 1, "exp"), (31, 11, 2, "exp"), (32, 11, 2, "text"), (33, 11, 3, "image"), (511, 11, 4, "exp"),
         (512, 11, 4, "exp"), (513, 11, 4, "exp"), (5000, 1, 3, "exp"), (5000, 2, 5, "exp"), (20000, 8, 9, "text"),
         (65536, 11, 16, "exp"), (100000, 12, 33, "image"), (123457, 10, 100, "text"), (300000, 11, 1000, "exp"),
-        (777777, 11, 4096, "text"), (1 << 20, 12, 2176, "image")]):
+        (777777, 11, 4096, "text"), (1 << 20, 12, 2176, "image"),
+        (300000, 13, 64, "exp"), (500000, 14, 300, "text"), (400000, 15, 33, "image"), (1 << 20, 16, 1000, "exp"),
+        (4097, 16, 3, "text")]):
     FUZZ.append((N, n, M, kind, 1000 + i))
 
 
@@ -66,12 +68,38 @@ def test_fuzz_vs_oracle(N, n, M, kind, seed):
     _check_full(c, sym)
 
 
-def test_single_symbol_fill():
+@pytest.mark.parametrize("n", [11, 12, 16])
+def test_single_symbol_fill(n):
     f = np.zeros(256, dtype=np.uint32)
-    f[9] = 1 << 12
+    f[9] = 1 << n
     sym = np.full(100000, 9, dtype=np.uint8)
-    c = R.recoil_encode(sym, f, 12, 8)
+    c = R.recoil_encode(sym, f, n, 8)
     _check_full(c, sym)
+
+
+def test_n16_outputs_before_group_zero():
+    rng = np.random.default_rng(8)
+    hist = np.zeros(256, dtype=np.uint64)
+    hist[:200] = rng.integers(1, 5, size=200)
+    hist[7] = 10 ** 7
+    f = oracle.build_model(hist, 16)
+    rare = [s for s in range(256) if f[s] == 1]
+    sym = synth.table_bytes(50000, (f / f.sum()).tolist(), 4)
+    sym[:32] = rare[0]
+    for c in (R.recoil_encode(sym, f, 16, 1), R.recoil_encode(sym, f, 16, 5), R.recoil_partitioned_encode(sym, f, 16, 7)):
+        _check_full(c, sym)
+
+
+def test_n16_exp_stream_full_alphabet():
+    """tab:overhead-n-16's setting: 8-bit symbols at n = 16."""
+    sym = synth.exp_bytes(3_000_000, 10, 55)
+    f = oracle.build_model(synth.histogram(sym), 16)
+    for M in (1, 16, 2176):
+        c = R.recoil_encode(sym, f, 16, M)
+        assert c.tobytes() == oracle.recoil_encode(sym, f, 16, M)
+        _check_full(c, sym)
+    p = R.recoil_partitioned_encode(sym, f, 16, 500)
+    _check_full(p, sym)
 
 
 @pytest.mark.parametrize("P", [1, 7, 64, 2176])

@@ -115,6 +115,28 @@ def test_cpu_decoder_thread_invariance_and_oracle_tasks():
         assert (out[lo:hi + 1] == sym[lo:hi + 1]).all()
 
 
+def test_n16_outputs_before_group_zero():
+    """n = 16 and f(s_0) = 1: Eq. 3 emits before the first symbol is encoded (x = L >= f 2^16);
+    the decoder must read those words after group 0 (oracle: final refill pass)."""
+    rng = np.random.default_rng(8)
+    hist = np.zeros(256, dtype=np.uint64)
+    hist[:200] = rng.integers(1, 5, size=200)
+    hist[7] = 10 ** 7
+    f = oracle.build_model(hist, 16)
+    rare = [s for s in range(256) if f[s] == 1]
+    assert rare
+    sym = synth.table_bytes(50000, (f / f.sum()).tolist(), 4)
+    sym[:32] = rare[0]  # every lane starts with an f = 1 symbol
+    words, fin, ev, _ = oracle.interleaved_encode(sym, f, 16, 32)
+    assert (ev["idx"] < 0).sum() == 32  # 32 emissions before group 0
+    for M in (1, 5):
+        c = R.recoil_encode(sym, f, 16, M)
+        assert c.tobytes() == oracle.recoil_encode(sym, f, 16, M)
+        assert (R.recoil_decode_cpu(c) == sym).all()
+    p = R.recoil_partitioned_encode(sym, f, 16, 7)
+    assert (R.recoil_decode_cpu(p) == sym).all()
+
+
 def test_single_symbol_and_tiny_streams():
     f = np.zeros(256, dtype=np.uint32)
     f[200] = 1 << 11
@@ -177,6 +199,7 @@ def test_decoder_plan_layout():
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 2 * len(sym) / 64
     c16 = R.recoil_encode(sym, oracle.build_model(synth.histogram(sym), 16), 16, 4)
-    with pytest.raises(R.RecoilError) as e:
-        R.recoil_decoder_create(c16)
-    assert e.value.rc == R.RECOIL_E_UNSUPPORTED
+    h = R.recoil_decoder_create(c16)  # n = 16: split-table LUT (2^16 symbol bytes + f, F)
+    p16 = R.recoil_decoder_plan(h)
+    assert p16["prob_bits"] == 16 and p16["workspace_bytes"] >= (1 << 16) + 1024
+    R.recoil_decoder_destroy(h)
