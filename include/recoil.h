@@ -182,6 +182,45 @@ void recoil_decoder_destroy(recoil_decoder *dec);
 int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);  /* 1 <= n <= 16 */
 
 /* ---------------------------------------------------------------------- */
+/* End-to-end pipelined decode on one GPU (host container -> host symbols)  */
+/* ---------------------------------------------------------------------- */
+
+typedef struct recoil_pipeline recoil_pipeline;
+
+/* Cut the container's tasks [task_begin, task_end) (UINT64_MAX: all) into
+ * n_chunks contiguous ranges of ~equal committed symbols (as recoil_shard_plan).  The container bytes must stay
+ * valid while the handle is used (its words are copied from them; pinned
+ * memory lets those copies run asynchronously).  Owns pinned host staging
+ * and CUDA events.  Errors: container errors, E_ARG, E_NOMEM, E_CUDA. */
+int recoil_pipeline_create(const uint8_t *container, uint64_t len, uint64_t task_begin, uint64_t task_end,
+                           uint32_t n_chunks, recoil_pipeline **out);
+
+/* Device scratch the caller must provide to recoil_pipeline_run with
+ * n_streams streams (1 <= n_streams <= 8): one buffer set per stream. */
+int recoil_pipeline_device_bytes(const recoil_pipeline *p, uint32_t n_streams, uint64_t *bytes);
+
+/* One end-to-end decode: per chunk k, on streams[k % n_streams], the host
+ * expands the chunk's tasks (a1), then H2D of LUT + task table (from pinned
+ * staging) and of the chunk's word slice, the decode kernel, and D2H of the
+ * chunk's symbols into host_out[out_lo, out_hi) (absolute symbol indices:
+ * host_out is indexed from symbol 0) and of its status word.
+ * Copies of one chunk overlap the kernels / copies of the others.  Returns
+ * once everything is enqueued; call recoil_pipeline_status to wait.
+ * host_out: N bytes (pinned for asynchronous copies).  Errors: E_ARG, E_CUDA,
+ * container errors. */
+int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t *host_out, void *const *streams,
+                        uint32_t n_streams);
+
+/* Synchronise the streams and fold the chunks' status words (as
+ * recoil_decoder_status).  *bad_task (may be NULL): first failing task. */
+int recoil_pipeline_status(recoil_pipeline *p, void *const *streams, uint32_t n_streams, uint64_t *bad_task);
+
+/* Kernel launches of the last run. */
+int recoil_pipeline_launches(const recoil_pipeline *p);
+
+void recoil_pipeline_destroy(recoil_pipeline *p);
+
+/* ---------------------------------------------------------------------- */
 /* Multi-GPU sharding (host planning; each GPU decodes its own task range) */
 /* ---------------------------------------------------------------------- */
 

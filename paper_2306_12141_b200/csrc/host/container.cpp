@@ -45,11 +45,21 @@ struct BitReader {
   const uint8_t *buf;
   uint64_t nbits;
   uint64_t pos = 0;
+  // MSB-first read of n <= 33 bits: one unaligned big-endian 64-bit load when
+  // 8 bytes are available, else byte by byte at the end of the buffer.
   bool get(uint32_t n, uint64_t *v) {
     if (pos + n > nbits) return false;
-    uint64_t r = 0;
-    for (uint32_t k = 0; k < n; ++k, ++pos) r = (r << 1) | ((buf[pos >> 3] >> (7 - (pos & 7))) & 1);
-    *v = r;
+    const uint64_t byte = pos >> 3;
+    uint64_t word;
+    if (byte + 8 <= (nbits + 7) >> 3) {
+      std::memcpy(&word, buf + byte, 8);
+      word = __builtin_bswap64(word);
+    } else {
+      word = 0;
+      for (uint64_t k = 0; k < 8; ++k) word = (word << 8) | (byte + k < ((nbits + 7) >> 3) ? buf[byte + k] : 0);
+    }
+    *v = n ? (word << (pos & 7)) >> (64 - n) : 0;
+    pos += n;
     return true;
   }
 };
@@ -183,14 +193,29 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o) {
   o->state.resize(P * W);
   o->gdiff.resize(P * W);
   int64_t dv[32];
+  static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "container words/states are little endian");
   for (uint64_t k = 0; k < P; ++k) {
-    if (pos + 2ull * W > len) return RECOIL_E_TRUNCATED;
-    for (uint32_t j = 0; j < W; ++j) o->state[k * W + j] = (uint16_t)get_le(c + pos + 2 * j, 2);
+    if (pos + 2ull * W + 1 > len) return RECOIL_E_TRUNCATED;
+    std::memcpy(&o->state[k * W], c + pos, 2ull * W);  // W x u16 LE anchor states
     pos += 2ull * W;
-    BitReader pr{c + pos, 8 * (len - pos)};
-    if (!get_series(&pr, dv, W, false, 4)) return RECOIL_E_TRUNCATED;
-    for (uint32_t j = 0; j < W; ++j) o->gdiff[k * W + j] = (uint16_t)dv[j];
-    pos += (pr.pos + 7) / 8;
+    // unsigned series, 4-bit width field: all W elements share one width w <= 16
+    const uint32_t w = (c[pos] >> 4) + 1;
+    const uint64_t bits = 4 + (uint64_t)W * w, bytes = (bits + 7) / 8;
+    if (pos + bytes > len) return RECOIL_E_TRUNCATED;
+    uint16_t *gd = &o->gdiff[k * W];
+    if (pos + bytes + 8 <= len) {  // fast path: one unaligned big-endian load per element
+      for (uint32_t j = 0; j < W; ++j) {
+        const uint64_t bp = 4 + (uint64_t)j * w;
+        uint64_t word;
+        std::memcpy(&word, c + pos + (bp >> 3), 8);
+        gd[j] = (uint16_t)((__builtin_bswap64(word) << (bp & 7)) >> (64 - w));
+      }
+    } else {
+      BitReader pr{c + pos, 8 * (len - pos)};
+      if (!get_series(&pr, dv, W, false, 4)) return RECOIL_E_TRUNCATED;
+      for (uint32_t j = 0; j < W; ++j) gd[j] = (uint16_t)dv[j];
+    }
+    pos += bytes;
   }
   o->meta_bytes = pos - meta_start;
   if (len < pos + 2 * o->B) return RECOIL_E_TRUNCATED;
@@ -198,13 +223,24 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o) {
   o->words = c + pos;
   // consistency: points inside the stream, sync starts strictly increasing
   int64_t prev_ss = -1;
+  o->sync_start.resize(P);
+  o->bidx.resize(P);
   for (uint64_t k = 0; k < P; ++k) {
     if (o->offset[k] >= o->B || o->maxg[k] >= o->G) return RECOIL_E_INCONSISTENT;
-    for (uint32_t j = 0; j < W; ++j)
-      if (o->gdiff[k * W + j] > o->maxg[k]) return RECOIL_E_INCONSISTENT;
-    int64_t ss, bi;
-    point_span(*o, k, &ss, &bi);
+    // anchor index of lane j = (maxg - d_j) W + j: its min / max over lanes via d_j W - j
+    const uint16_t *gd = &o->gdiff[k * W];
+    int32_t dmax = 0, vmax = INT32_MIN, vmin = INT32_MAX;
+    for (uint32_t j = 0; j < W; ++j) {
+      const int32_t v = (int32_t)gd[j] * (int32_t)W - (int32_t)j;
+      dmax = std::max(dmax, (int32_t)gd[j]);
+      vmax = std::max(vmax, v);
+      vmin = std::min(vmin, v);
+    }
+    if ((uint64_t)dmax > o->maxg[k]) return RECOIL_E_INCONSISTENT;
+    const int64_t ss = (int64_t)o->maxg[k] * W - vmax, bi = (int64_t)o->maxg[k] * W - vmin;
     if ((uint64_t)bi >= o->N || ss <= prev_ss) return RECOIL_E_INCONSISTENT;
+    o->sync_start[k] = ss;
+    o->bidx[k] = bi;
     prev_ss = ss;
   }
   return RECOIL_OK;

@@ -19,7 +19,7 @@ struct Tables {
 };
 
 int decode_task(const Decoder &d, const Tables &tb, const TaskRec &t, const uint16_t *w, uint8_t *out) {
-  const uint32_t n = d.c.n, mask = (1u << n) - 1;
+  const uint32_t n = d.c->n, mask = (1u << n) - 1;
   uint32_t x[32], st[32];
   int32_t ig[32];
   bool inited[32];
@@ -77,29 +77,29 @@ extern "C" int recoil_decode_cpu(const uint8_t *container, uint64_t len, uint8_t
     Decoder d;
     int rc = build_decoder(container, len, 0, UINT64_MAX, &d, false);
     if (rc) return rc;
-    if (d.c.N == 0) return RECOIL_OK;
+    if (d.c->N == 0) return RECOIL_OK;
     if (!out) return RECOIL_E_ARG;
     if (d.single_symbol >= 0) {
-      std::memset(out, d.single_symbol, d.c.N);
+      std::memset(out, d.single_symbol, d.c->N);
       return RECOIL_OK;
     }
     Tables tb;
-    const uint32_t n = d.c.n;
+    const uint32_t n = d.c->n;
     tb.sym.resize(1u << n);
     tb.f.resize(1u << n);
     tb.bias.resize(1u << n);
     uint32_t F = 0;
     for (uint32_t s = 0; s < 256; ++s) {
-      for (uint32_t k = 0; k < d.c.f[s]; ++k) {
+      for (uint32_t k = 0; k < d.c->f[s]; ++k) {
         tb.sym[F + k] = (uint8_t)s;
-        tb.f[F + k] = d.c.f[s];
+        tb.f[F + k] = d.c->f[s];
         tb.bias[F + k] = k;
       }
-      F += d.c.f[s];
+      F += d.c->f[s];
     }
     // the container's words as a host u16 array (little-endian host)
-    std::vector<uint16_t> w(d.c.B + 1);
-    if (d.c.B) std::memcpy(w.data(), d.c.words, 2 * d.c.B);
+    std::vector<uint16_t> w(d.c->B + 1);
+    if (d.c->B) std::memcpy(w.data(), d.c->words, 2 * d.c->B);
     const uint16_t *slice = w.data() + d.plan.word_lo;
     if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
     threads = std::min<uint32_t>(threads, (uint32_t)std::max<size_t>(1, d.tasks.size()));

@@ -45,9 +45,16 @@ static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
                   bool for_gpu) {
-  int rc = parse_container(cbytes, len, &d->c);
+  auto parsed = std::make_shared<Container>();
+  int rc = parse_container(cbytes, len, parsed.get());
   if (rc) return rc;
-  const Container &c = d->c;
+  return build_decoder_from(std::move(parsed), task_begin, task_end, d, for_gpu);
+}
+
+int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begin, uint64_t task_end, Decoder *d,
+                       bool for_gpu) {
+  d->c = std::move(cptr);
+  const Container &c = *d->c;
   if (task_end > c.M) task_end = c.M;
   if (task_begin > task_end) return RECOIL_E_ARG;
   if (for_gpu && c.n > kMaxGpuProbBits) return RECOIL_E_UNSUPPORTED;
@@ -71,16 +78,11 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
     std::memset(&r, 0, sizeof(r));
     r.task_id = (uint32_t)t;
     if (!c.partitioned) {
-      int64_t ss, bi;
-      uint64_t lo = 0;
-      if (t > 0) {
-        point_span(c, t - 1, &ss, &bi);
-        lo = (uint64_t)ss;
-      }
+      const uint64_t lo = t > 0 ? (uint64_t)c.sync_start[t - 1] : 0;
       r.commit_lo = lo;
       r.end_cursor = lo == 0 ? -1 : kNoEndCheck;
       if (t + 1 < c.M) {
-        point_span(c, t, &ss, &bi);
+        const int64_t ss = c.sync_start[t];
         r.commit_hi = (uint64_t)ss - 1;
         r.write_hi = kLanes * ((uint64_t)ss / kLanes + 1);  // through the sync completion group
         r.cursor0 = (int64_t)c.offset[t];
@@ -131,10 +133,8 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
     } else if (task_begin >= 2) {
       // task a reads no word below offset(point a-2) - 31 when sync_start(point a-1) >
       // boundary(point a-2) (reading Z9, enforced by the encoder); else start at 0.
-      int64_t ss1, bi1, ss2, bi2;
-      point_span(c, task_begin - 1, &ss1, &bi1);
-      point_span(c, task_begin - 2, &ss2, &bi2);
-      if (ss1 > bi2 && c.offset[task_begin - 2] >= kLanes - 1) word_lo = c.offset[task_begin - 2] - (kLanes - 1);
+      if (c.sync_start[task_begin - 1] > c.bidx[task_begin - 2] && c.offset[task_begin - 2] >= kLanes - 1)
+        word_lo = c.offset[task_begin - 2] - (kLanes - 1);
     }
   }
   word_lo &= ~(uint64_t)(kChunkWords - 1);
@@ -150,12 +150,6 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
     p.out_lo = d->tasks.front().commit_lo;
     p.out_hi = d->tasks.back().commit_hi + 1;
   }
-  // Longest task first: the persistent warps take tasks in table order, so the
-  // kernel's tail is made of the shortest tasks (LPT order).  Output positions
-  // are per task, so the order does not change the result.
-  std::stable_sort(d->tasks.begin(), d->tasks.end(), [](const TaskRec &a, const TaskRec &b) {
-    return a.start_group - (int64_t)(a.commit_lo / kLanes) > b.start_group - (int64_t)(b.commit_lo / kLanes);
-  });
   p.out_base = p.out_lo & ~(uint64_t)(kBlockBytes - 1);
   uint64_t write_end = p.out_hi;
   for (const TaskRec &r : d->tasks) write_end = std::max(write_end, r.write_hi);
@@ -198,33 +192,44 @@ extern "C" int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan)
 
 extern "C" void recoil_decoder_destroy(recoil_decoder *dec) { delete reinterpret_cast<Decoder *>(dec); }
 
+namespace recoil {
+
+void shard_bounds_range(const Container &c, uint64_t tb, uint64_t te, uint32_t n_shards, uint64_t *bounds) {
+  // commit_lo of every task; shard s starts at the first task whose commit_lo reaches
+  // lo(tb) + s (lo(te) - lo(tb)) / n
+  auto lo_of = [&](uint64_t t) -> uint64_t {
+    if (t >= c.M) return c.N;
+    if (c.partitioned) return kLanes * (t * c.G / c.M);
+    return t == 0 ? 0 : (uint64_t)c.sync_start[t - 1];
+  };
+  te = std::min<uint64_t>(te, c.M);
+  tb = std::min(tb, te);
+  std::vector<uint64_t> lo(te - tb);
+  for (uint64_t t = tb; t < te; ++t) lo[t - tb] = lo_of(t);
+  const uint64_t a = lo_of(tb), span = lo_of(te) - a;
+  bounds[0] = tb;
+  for (uint32_t s = 1; s < n_shards; ++s) {
+    uint64_t target = a + ceil_div((uint64_t)s * span, n_shards);
+    uint64_t b = tb + (uint64_t)(std::lower_bound(lo.begin(), lo.end(), target) - lo.begin());
+    bounds[s] = std::max(bounds[s - 1], std::min<uint64_t>(b, te));
+  }
+  bounds[n_shards] = te;
+}
+
+void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds) {
+  shard_bounds_range(c, 0, c.M, n_shards, bounds);
+}
+
+}  // namespace recoil
+
 extern "C" int recoil_shard_plan(const uint8_t *container, uint64_t len, uint32_t n_shards,
                                  uint64_t *bounds) {
   if (!container || !bounds || n_shards < 1) return RECOIL_E_ARG;
   try {
-    Container c;
-    int rc = parse_container(container, len, &c);
+    recoil::Container c;
+    int rc = recoil::parse_container(container, len, &c);
     if (rc) return rc;
-    // commit_lo of every task; shard d starts at the first task whose commit_lo >= d N / D
-    std::vector<uint64_t> lo(c.M);
-    for (uint64_t t = 0; t < c.M; ++t) {
-      if (c.partitioned) {
-        lo[t] = kLanes * (t * c.G / c.M);
-      } else if (t == 0) {
-        lo[t] = 0;
-      } else {
-        int64_t ss, bi;
-        point_span(c, t - 1, &ss, &bi);
-        lo[t] = (uint64_t)ss;
-      }
-    }
-    bounds[0] = 0;
-    for (uint32_t s = 1; s < n_shards; ++s) {
-      uint64_t target = ceil_div((uint64_t)s * c.N, n_shards);
-      uint64_t b = (uint64_t)(std::lower_bound(lo.begin(), lo.end(), target) - lo.begin());
-      bounds[s] = std::max(bounds[s - 1], std::min<uint64_t>(b, c.M));
-    }
-    bounds[n_shards] = c.M;
+    recoil::shard_bounds(c, n_shards, bounds);
     return RECOIL_OK;
   } catch (const std::bad_alloc &) {
     return RECOIL_E_NOMEM;

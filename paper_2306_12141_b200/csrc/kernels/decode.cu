@@ -472,8 +472,8 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   if (!d->tasks.empty() && cudaMemcpyAsync(ws + d->tasks_off, d->tasks.data(), sizeof(TaskRec) * d->tasks.size(),
                                            cudaMemcpyHostToDevice, s) != cudaSuccess)
     return RECOIL_E_CUDA;
-  uint64_t have = d->c.B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c.B - p.word_lo) : 0;
-  if (have && cudaMemcpyAsync(d_words, d->c.words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
+  uint64_t have = d->c->B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c->B - p.word_lo) : 0;
+  if (have && cudaMemcpyAsync(d_words, d->c->words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
                   cudaSuccess)
     return RECOIL_E_CUDA;
   if (p.word_count > have && cudaMemsetAsync(d_words + have, 0, 2 * (p.word_count - have), s) != cudaSuccess)

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "recoil.h"
@@ -30,6 +31,7 @@ struct Container {
   std::vector<uint64_t> maxg;     // Recoil: M-1 anchor (max) group IDs
   std::vector<uint16_t> state;    // Recoil: (M-1) x W anchor states (< L)
   std::vector<uint16_t> gdiff;    // Recoil: (M-1) x W group differences to the anchor
+  std::vector<int64_t> sync_start, bidx;  // Recoil: per point min / max anchor index (filled by parse)
   std::vector<uint64_t> part_words; // partitioned: M word counts
   const uint8_t *words = nullptr; // B little-endian u16
   uint64_t header_bytes = 0, meta_bytes = 0, total_bytes = 0;
@@ -72,7 +74,7 @@ struct DeviceStatus {   // first 16 B of the workspace, zeroed before every deco
 
 // Host-side decode plan (the recoil_decoder handle).
 struct Decoder {
-  Container c;
+  std::shared_ptr<const Container> c;  // parsed container (shared by the chunks of a pipeline)
   recoil_plan plan{};
   std::vector<uint8_t> lut;        // n <= 12: 2^n packed u32 s | bias << 8 | f << 20;
                                    // n >= 13: 2^n symbol bytes + 256 x u32 (f | F << 16)
@@ -85,6 +87,13 @@ struct Decoder {
 
 int build_decoder(const uint8_t *c, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
                   bool for_gpu);
+// Plan tasks [task_begin, task_end) of an already parsed container.
+int build_decoder_from(std::shared_ptr<const Container> c, uint64_t task_begin, uint64_t task_end, Decoder *d,
+                       bool for_gpu);
+// Contiguous task ranges with ~equal committed symbols (recoil_shard_plan).
+void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
+void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,
+                        uint64_t *bounds);
 void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
 
 

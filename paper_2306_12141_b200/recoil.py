@@ -32,6 +32,8 @@ EXPORTS = [
     "recoil_partitioned_encode", "recoil_decoder_create", "recoil_decoder_plan", "recoil_decoder_upload",
     "recoil_decode", "recoil_decoder_status", "recoil_decoder_launches", "recoil_decoder_destroy",
     "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu",
+    "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
+    "recoil_pipeline_launches", "recoil_pipeline_destroy",
 ]
 
 
@@ -89,6 +91,12 @@ def load(path: str = LIB_PATH):
         "recoil_decode_occupancy": (i32, [i32, u32, P, P]),
         "recoil_shard_plan": (i32, [P, u64, u32, P]),
         "recoil_decode_cpu": (i32, [P, u64, P, u32]),
+        "recoil_pipeline_create": (i32, [P, u64, u64, u64, u32, P]),
+        "recoil_pipeline_device_bytes": (i32, [P, u32, P]),
+        "recoil_pipeline_run": (i32, [P, P, P, P, u32]),
+        "recoil_pipeline_status": (i32, [P, P, u32, P]),
+        "recoil_pipeline_launches": (i32, [P]),
+        "recoil_pipeline_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -272,6 +280,83 @@ class GpuDecoder:
 
     def close(self) -> None:
         recoil_decoder_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.close()
+        except Exception:
+            pass
+
+
+def recoil_pipeline_create(container, n_chunks: int, task_begin: int = 0,
+                           task_end: int = (1 << 64) - 1) -> ctypes.c_void_p:
+    c = _u8(container)
+    h = ctypes.c_void_p()
+    _check(load().recoil_pipeline_create(c.ctypes.data, c.size, task_begin, task_end, n_chunks, ctypes.byref(h)),
+           "recoil_pipeline_create")
+    return h
+
+
+def recoil_pipeline_device_bytes(handle, n_streams: int) -> int:
+    b = ctypes.c_uint64(0)
+    _check(load().recoil_pipeline_device_bytes(handle, n_streams, ctypes.byref(b)), "recoil_pipeline_device_bytes")
+    return b.value
+
+
+def _streams(streams):
+    arr = (ctypes.c_void_p * len(streams))(*[s for s in streams])
+    return arr, len(streams)
+
+
+def recoil_pipeline_run(handle, d_scratch: int, host_out: int, streams) -> None:
+    arr, n = _streams(streams)
+    _check(load().recoil_pipeline_run(handle, d_scratch, host_out, arr, n), "recoil_pipeline_run")
+
+
+def recoil_pipeline_status(handle, streams) -> tuple[int, int | None]:
+    arr, n = _streams(streams)
+    bad = ctypes.c_uint64(0)
+    rc = load().recoil_pipeline_status(handle, arr, n, ctypes.byref(bad))
+    return rc, (None if bad.value == (1 << 64) - 1 else bad.value)
+
+
+def recoil_pipeline_launches(handle) -> int:
+    return _check(load().recoil_pipeline_launches(handle), "recoil_pipeline_launches")
+
+
+def recoil_pipeline_destroy(handle) -> None:
+    if handle:
+        load().recoil_pipeline_destroy(handle)
+
+
+class HostPipeline:
+    """End-to-end host->host decode on one GPU (recoil_pipeline_*): owns the handle,
+    the torch device scratch and the CUDA streams.  ``container`` should be pinned."""
+
+    def __init__(self, container, device: int = 0, n_chunks: int = 8, n_streams: int = 3, task_begin: int = 0,
+                 task_end: int = (1 << 64) - 1):
+        import torch
+        self.container = _u8(container)
+        self.device = torch.device("cuda", device)
+        self.handle = recoil_pipeline_create(self.container, n_chunks, task_begin, task_end)
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(n_streams)]
+        self.scratch = torch.empty(max(recoil_pipeline_device_bytes(self.handle, n_streams), 256),
+                                   dtype=torch.uint8, device=self.device)
+
+    def run(self, host_out) -> None:
+        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
+        recoil_pipeline_run(self.handle, self.scratch.data_ptr(), ptr, [s.cuda_stream for s in self.streams])
+
+    def status(self):
+        return recoil_pipeline_status(self.handle, [s.cuda_stream for s in self.streams])
+
+    def launches(self) -> int:
+        return recoil_pipeline_launches(self.handle)
+
+    def close(self) -> None:
+        recoil_pipeline_destroy(self.handle)
         self.handle = None
 
     def __del__(self):

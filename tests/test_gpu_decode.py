@@ -130,6 +130,37 @@ def test_sharded_task_ranges(shards):
         assert covered == len(sym) and (got == sym).all()
 
 
+@pytest.mark.parametrize("chunks,streams", [(1, 1), (5, 2), (8, 3), (64, 8)])
+def test_host_pipeline_end_to_end(chunks, streams):
+    """recoil_pipeline_*: host container -> host symbols over chunked task ranges on
+    several streams (and a task sub-range, as one rank of a multi-GPU job)."""
+    sym = synth.text_bytes(6_000_000, 31)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 3000)
+    pinned = torch.empty(len(c), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = c
+    out = torch.zeros(len(sym), dtype=torch.uint8, pin_memory=True)
+    pipe = R.HostPipeline(pinned.numpy(), 0, n_chunks=chunks, n_streams=streams)
+    for _ in range(2):
+        out.zero_()
+        pipe.run(out)
+        rc, bad = pipe.status()
+        assert rc == 0, (rc, bad)
+        assert (out.numpy() == sym).all()
+    pipe.close()
+    bounds = R.recoil_shard_plan(c, 3)
+    out.zero_()
+    pipe = R.HostPipeline(pinned.numpy(), 0, n_chunks=chunks, n_streams=streams, task_begin=bounds[1],
+                          task_end=bounds[2])
+    pipe.run(out)
+    assert pipe.status()[0] == 0
+    h = R.recoil_decoder_create(c, bounds[1], bounds[2])
+    p = R.recoil_decoder_plan(h)
+    R.recoil_decoder_destroy(h)
+    assert (out.numpy()[p["out_lo"]:p["out_hi"]] == sym[p["out_lo"]:p["out_hi"]]).all()
+    pipe.close()
+
+
 def test_combined_containers_decode_identically():
     sym = synth.exp_bytes(4_000_000, 50, 88)
     f = oracle.build_model(synth.histogram(sym), 11)

@@ -184,6 +184,7 @@ def test_decoder_plan_layout():
     assert p["n_tasks"] == 64 and p["word_lo"] == 0 and p["word_count"] % 256 == 0
     assert p["word_count"] >= R.recoil_inspect(c)["n_words"]
     assert (p["out_lo"], p["out_hi"], p["out_base"]) == (0, len(sym), 0)
+    assert p["out_count"] == (len(sym) + 15) // 16 * 16
     R.recoil_decoder_destroy(h)
     bounds = R.recoil_shard_plan(c, 4)
     assert bounds[0] == 0 and bounds[-1] == 64 and bounds == sorted(bounds)
@@ -192,6 +193,7 @@ def test_decoder_plan_layout():
         h = R.recoil_decoder_create(c, a, b)
         p = R.recoil_decoder_plan(h)
         assert p["word_lo"] % 256 == 0 and p["out_base"] % 512 == 0 and p["out_base"] <= p["out_lo"]
+        assert p["out_count"] >= p["out_hi"] - p["out_base"] and p["out_count"] % 16 == 0
         spans.append((p["out_lo"], p["out_hi"]))
         R.recoil_decoder_destroy(h)
     assert spans[0][0] == 0 and spans[-1][1] == len(sym)
