@@ -3,4 +3,4 @@
 OUT=$1; shift
 cd "$(dirname "$0")/.." && mkdir -p build_var
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Iinclude "$@" -c paper_2306_12141_b200/csrc/kernels/decode.cu -o build_var/decode_var.o
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT build_var/decode_var.o paper_2306_12141_b200/build/container.cpp.o paper_2306_12141_b200/build/cpu_decode.cpp.o paper_2306_12141_b200/build/encode.cpp.o paper_2306_12141_b200/build/plan.cpp.o -lpthread
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT build_var/decode_var.o paper_2306_12141_b200/build/*.cpp.o -lpthread
