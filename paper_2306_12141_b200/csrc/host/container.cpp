@@ -145,13 +145,14 @@ void point_span(const Container &c, uint64_t k, int64_t *sync_start, int64_t *bi
   *bidx = mx;
 }
 
-int parse_container(const uint8_t *c, uint64_t len, Container *o) {
+int parse_container(const uint8_t *c, uint64_t len, Container *o, bool light) {
   if (!c || len < 28) return c ? RECOIL_E_TRUNCATED : RECOIL_E_ARG;
   bool part = std::memcmp(c, "RCV1", 4) == 0;
   if (!part && std::memcmp(c, "RCL1", 4) != 0) return RECOIL_E_BAD_MAGIC;
   if (c[4] != 1 || c[5] != 8) return RECOIL_E_VERSION;
   *o = Container();
   o->partitioned = part;
+  o->bytes = c;
   o->n = c[6];
   o->W = c[7];
   o->M = (uint32_t)get_le(c + 8, 4);
@@ -190,6 +191,25 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o) {
   o->maxg.resize(P);
   for (uint64_t k = 1; k <= P; ++k) o->maxg[k - 1] = (uint64_t)((int64_t)(k * Eg) + d[k - 1]);
   pos += (br.pos + 7) / 8;
+  if (light) {  // record offsets only: record k = W u16 states + 1 width byte + 4 w bytes of series
+    o->light = true;
+    o->rec_off.resize(P + 1);
+    for (uint64_t k = 0; k < P; ++k) {
+      o->rec_off[k] = pos;
+      if (pos + 2ull * W + 1 > len) return RECOIL_E_TRUNCATED;
+      const uint32_t w = (c[pos + 2ull * W] >> 4) + 1;
+      pos += 2ull * W + (4 + (uint64_t)W * w + 7) / 8;
+    }
+    o->rec_off[P] = pos;
+    o->meta_bytes = pos - meta_start;
+    if (len < pos + 2 * o->B) return RECOIL_E_TRUNCATED;
+    if (len != pos + 2 * o->B) return RECOIL_E_INCONSISTENT;
+    o->words = c + pos;
+    for (uint64_t k = 0; k < P; ++k)
+      if (o->offset[k] >= o->B || o->maxg[k] >= o->G || (k && o->offset[k] <= o->offset[k - 1]))
+        return RECOIL_E_INCONSISTENT;
+    return RECOIL_OK;
+  }
   o->state.resize(P * W);
   o->gdiff.resize(P * W);
   int64_t dv[32];
@@ -243,6 +263,28 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o) {
     o->bidx[k] = bi;
     prev_ss = ss;
   }
+  return RECOIL_OK;
+}
+
+int point_span_light(const Container &c, uint64_t k, int64_t *sync_start, int64_t *bidx) {
+  if (!c.light) {
+    *sync_start = c.sync_start[k];
+    *bidx = c.bidx[k];
+    return RECOIL_OK;
+  }
+  const uint8_t *r = c.bytes + c.rec_off[k] + 2 * c.W;
+  BitReader br{r, 8 * (c.rec_off[k + 1] - c.rec_off[k] - 2 * c.W)};
+  int64_t d[32];
+  if (!get_series(&br, d, c.W, false, 4)) return RECOIL_E_TRUNCATED;
+  int64_t mn = INT64_MAX, mx = -1;
+  for (uint32_t j = 0; j < c.W; ++j) {
+    if ((uint64_t)d[j] > c.maxg[k]) return RECOIL_E_INCONSISTENT;
+    const int64_t idx = (int64_t)(c.maxg[k] - (uint64_t)d[j]) * c.W + j;
+    mn = std::min(mn, idx);
+    mx = std::max(mx, idx);
+  }
+  *sync_start = mn;
+  *bidx = mx;
   return RECOIL_OK;
 }
 

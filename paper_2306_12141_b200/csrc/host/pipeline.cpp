@@ -71,7 +71,7 @@ extern "C" int recoil_pipeline_create(const uint8_t *container, uint64_t len, ui
   *out = nullptr;
   try {
     auto c = std::make_shared<Container>();
-    int rc = parse_container(container, len, c.get());
+    int rc = parse_container(container, len, c.get(), /*light=*/true);
     if (rc) return rc;
     Pipeline *pl = new Pipeline();
     pl->bytes = container;
@@ -119,7 +119,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
   try {
     // per run: parse and plan again (this is the host half of the path)
     auto c = std::make_shared<Container>();
-    int rc = parse_container(pl->bytes, pl->len, c.get());
+    int rc = parse_container(pl->bytes, pl->len, c.get(), /*light=*/true);
     if (rc) return rc;
     pl->bounds.assign(pl->chunks + 1, 0);
     shard_bounds_range(*c, pl->task_begin, pl->task_end, pl->chunks, pl->bounds.data());
@@ -154,8 +154,13 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (!d.lut.empty()) std::memcpy(stg + d.lut_off, d.lut.data(), d.lut.size());
       if (!d.finals.empty()) std::memcpy(stg + d.finals_off, d.finals.data(), 4 * d.finals.size());
       if (!d.tasks.empty()) std::memcpy(stg + d.tasks_off, d.tasks.data(), sizeof(TaskRec) * d.tasks.size());
-      if (cudaMemcpyAsync(ws, stg, pn.workspace_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      if (!d.heads.empty()) std::memcpy(stg + d.tasks_off, d.heads.data(), sizeof(TaskHead) * d.heads.size());
+      const uint64_t staged_bytes = d.fused ? d.rec_off : pn.workspace_bytes;  // raw records: from the container
+      if (cudaMemcpyAsync(ws, stg, staged_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaEventRecord(pl->staged[s], st) != cudaSuccess)
+        return RECOIL_E_CUDA;
+      if (d.rec_len && cudaMemcpyAsync(ws + d.rec_off, c->bytes + d.rec_src, d.rec_len, cudaMemcpyHostToDevice,
+                                       st) != cudaSuccess)
         return RECOIL_E_CUDA;
       const uint64_t have = c->B > pn.word_lo ? std::min<uint64_t>(pn.word_count, c->B - pn.word_lo) : 0;
       if (have && cudaMemcpyAsync(words, c->words + 2 * pn.word_lo, 2 * have, cudaMemcpyHostToDevice, st) !=
@@ -190,7 +195,8 @@ extern "C" int recoil_pipeline_status(recoil_pipeline *p, void *const *streams, 
   for (uint32_t k = 0; k < pl->chunks && k < pl->dec.size(); ++k) {
     const DeviceStatus &st = pl->status[k];
     if (st.bad_task) bad = std::min<uint64_t>(bad, 0xFFFFFFFFu - st.bad_task);
-    if (st.flags & 1u) rc = RECOIL_E_UNDERFLOW;
+    if (st.flags & 4u) rc = RECOIL_E_INCONSISTENT;
+    else if ((st.flags & 1u) && rc != RECOIL_E_INCONSISTENT) rc = RECOIL_E_UNDERFLOW;
     else if ((st.flags & 2u) && rc == RECOIL_OK) rc = RECOIL_E_SYNC;
   }
   if (bad_task) *bad_task = bad;

@@ -46,15 +46,115 @@ static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
                   bool for_gpu) {
   auto parsed = std::make_shared<Container>();
-  int rc = parse_container(cbytes, len, parsed.get());
+  int rc = parse_container(cbytes, len, parsed.get(), /*light=*/for_gpu);
   if (rc) return rc;
   return build_decoder_from(std::move(parsed), task_begin, task_end, d, for_gpu);
+}
+
+// Recoil on the GPU: task heads only (row a1 split: the O(M) global series and
+// record offsets are decoded here, the per-lane anchors in the kernel).
+static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
+  const Container &c = *d->c;
+  d->fused = true;
+  pack_lut(c.f, c.n, &d->lut);
+  d->finals = c.finals;
+  d->heads.clear();
+  d->tasks.clear();
+  const uint64_t P = c.M - 1;
+  recoil_plan &p = d->plan;
+  std::memset(&p, 0, sizeof(p));
+  p.task_begin = tb;
+  p.task_end = te;
+  p.prob_bits = c.n;
+  uint64_t word_lo = 0, word_hi = 0;
+  int64_t ss, bi;
+  int rc;
+  for (uint64_t t = tb; t < te; ++t) {
+    if (c.N == 0) break;
+    TaskHead h;
+    std::memset(&h, 0, sizeof(h));
+    h.task_id = (uint32_t)t;
+    if (t < P) {
+      h.cursor0 = (int32_t)0;  // set below (slice relative)
+      h.start_group = (int32_t)c.maxg[t];
+    } else {
+      h.start_group = (int32_t)(c.G - 1);
+      h.flags |= kHeadLast;
+    }
+    if (t > 0)
+      h.maxg_prev = (uint32_t)c.maxg[t - 1];
+    else
+      h.flags |= kHeadFirst;
+    d->heads.push_back(h);
+  }
+  if (!d->heads.empty()) {
+    const uint64_t t_last = tb + d->heads.size() - 1;
+    word_hi = (t_last < P ? c.offset[t_last] : c.B - 1) + 1;
+    if (tb >= 2) {
+      int64_t ss1, bi1, ss2, bi2;
+      if ((rc = point_span_light(c, tb - 1, &ss1, &bi1)) || (rc = point_span_light(c, tb - 2, &ss2, &bi2))) return rc;
+      if (ss1 > bi2 && c.offset[tb - 2] >= kLanes - 1) word_lo = c.offset[tb - 2] - (kLanes - 1);
+    }
+    if (tb > 0) {
+      if ((rc = point_span_light(c, tb - 1, &ss, &bi))) return rc;
+      p.out_lo = (uint64_t)ss;
+    }
+    uint64_t write_end;
+    if (t_last < P) {
+      if ((rc = point_span_light(c, t_last, &ss, &bi))) return rc;
+      p.out_hi = (uint64_t)ss;
+      write_end = kLanes * ((uint64_t)ss / kLanes + 1);
+    } else {
+      p.out_hi = c.N;
+      write_end = (c.N + 15) & ~15ull;
+    }
+    p.out_base = p.out_lo & ~(uint64_t)(kBlockBytes - 1);
+    p.out_count = ((std::max(write_end, p.out_hi) + 15) & ~15ull) - p.out_base;
+  }
+  word_lo &= ~(uint64_t)(kChunkWords - 1);
+  word_hi = ceil_div(std::max(word_hi, word_lo + 1), kChunkWords) * kChunkWords;
+  if (word_hi - word_lo >= (1ull << 31)) return RECOIL_E_UNSUPPORTED;  // 32-bit slice cursor
+  p.word_lo = word_lo;
+  p.word_count = word_hi - word_lo;
+  // records needed: points [tb - 1, min(te, P)) (task t reads points t and t - 1)
+  const uint64_t r0 = tb > 0 ? tb - 1 : 0, r1 = std::min<uint64_t>(te, P);
+  d->rec_src = r1 > r0 ? c.rec_off[r0] : 0;
+  d->rec_len = r1 > r0 ? c.rec_off[r1] - c.rec_off[r0] : 0;
+  for (size_t i = 0; i < d->heads.size(); ++i) {
+    TaskHead &h = d->heads[i];
+    const uint64_t t = tb + i;
+    h.cursor0 = (int32_t)((t < P ? (int64_t)c.offset[t] : (int64_t)c.B - 1) - (int64_t)word_lo);
+    if (t < P) h.rec = (uint32_t)(c.rec_off[t] - d->rec_src);
+    if (t > 0) h.rec_prev = (uint32_t)(c.rec_off[t - 1] - d->rec_src);
+    if (h.flags & kHeadFirst) h.end_cursor = (int32_t)(-1 - (int64_t)word_lo);
+  }
+  d->n_tasks = (uint32_t)d->heads.size();
+  p.n_tasks = d->n_tasks;
+  d->lut_off = 16;
+  d->finals_off = align16(d->lut_off + d->lut.size());
+  d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
+  d->rec_off = align16(d->tasks_off + sizeof(TaskHead) * d->heads.size());
+  p.workspace_bytes = align16(d->rec_off + d->rec_len + 256);  // + over-read pad of the record windows
+  p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);
+  return RECOIL_OK;
 }
 
 int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begin, uint64_t task_end, Decoder *d,
                        bool for_gpu) {
   d->c = std::move(cptr);
   const Container &c = *d->c;
+  if (task_end > c.M) task_end = c.M;
+  if (task_begin > task_end) return RECOIL_E_ARG;
+  {
+    int present = 0;
+    for (int s = 0; s < 256; ++s)
+      if (c.f[s]) {
+        present++;
+        d->single_symbol = s;
+      }
+    if (present != 1) d->single_symbol = -1;
+  }
+  if (for_gpu && !c.partitioned && c.light) return build_fused(d, task_begin, task_end);
   if (task_end > c.M) task_end = c.M;
   if (task_begin > task_end) return RECOIL_E_ARG;
   if (for_gpu && c.n > kMaxGpuProbBits) return RECOIL_E_UNSUPPORTED;
@@ -157,6 +257,7 @@ int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begi
   d->lut_off = 16;
   d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
+  d->n_tasks = (uint32_t)d->tasks.size();
   p.workspace_bytes = align16(d->tasks_off + sizeof(TaskRec) * d->tasks.size());
   p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);
   return RECOIL_OK;
@@ -195,12 +296,13 @@ extern "C" void recoil_decoder_destroy(recoil_decoder *dec) { delete reinterpret
 namespace recoil {
 
 void shard_bounds_range(const Container &c, uint64_t tb, uint64_t te, uint32_t n_shards, uint64_t *bounds) {
-  // commit_lo of every task; shard s starts at the first task whose commit_lo reaches
-  // lo(tb) + s (lo(te) - lo(tb)) / n
+  // shard s starts at the first task whose start reaches lo(tb) + s (lo(te) - lo(tb)) / n
+  // balance on the anchor group of the entry point below each task (within one
+  // Synchronization Section of the committed start; available from a light parse)
   auto lo_of = [&](uint64_t t) -> uint64_t {
     if (t >= c.M) return c.N;
     if (c.partitioned) return kLanes * (t * c.G / c.M);
-    return t == 0 ? 0 : (uint64_t)c.sync_start[t - 1];
+    return t == 0 ? 0 : kLanes * c.maxg[t - 1];
   };
   te = std::min<uint64_t>(te, c.M);
   tb = std::min(tb, te);

@@ -50,7 +50,11 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 struct Params {
   const uint8_t *lut;     // n <= 12: 2^n packed u32; n >= 13: 2^n symbol bytes + 256 x u32 (f | F << 16)
   const uint32_t *finals;
-  const TaskRec *tasks;
+  const TaskRec *tasks;   // prebuilt records (partitioned containers)
+  const TaskHead *heads;  // fused a1 (Recoil): task heads ...
+  const uint8_t *recs;    // ... and the raw split records they point into
+  uint32_t N_lo, N_hi;    // N (symbols) as two words
+  int32_t G;              // symbol groups
   DeviceStatus *status;
   const uint16_t *words;  // slice base (stream word word_lo)
   uint8_t *out;           // symbol out_base
@@ -112,6 +116,26 @@ __device__ __forceinline__ uint32_t lanemask_gt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_gt;" : "=r"(m));
   return m;
+}
+
+// 4 bytes at byte offset `off` of a warp-distributed window (lane k holds bytes
+// [4k, 4k + 4) of it, little endian); off + 4 <= 128.
+__device__ __forceinline__ uint32_t window_u32(uint32_t win, uint32_t off) {
+  const uint32_t lo = __shfl_sync(kFull, win, (off >> 2) & 31), hi = __shfl_sync(kFull, win, ((off >> 2) + 1) & 31);
+  const uint32_t r = 8 * (off & 3);
+  return r ? (lo >> r) | (hi << (32 - r)) : lo;
+}
+// Element j of a W = 32 unsigned data series whose width field is
+// the high nibble of byte `base` of the window: w = field + 1 bits, MSB first.
+__device__ __forceinline__ uint32_t series_elem(uint32_t win, uint32_t base, uint32_t j, uint32_t *width) {
+  const uint32_t w = ((window_u32(win, base) >> 4) & 0xFu) + 1;
+  const uint32_t bit = 4 + j * w;
+  const uint32_t be = __byte_perm(window_u32(win, base + (bit >> 3)), 0, 0x0123);  // big endian
+  *width = w;
+  return (be << (bit & 7)) >> (32 - w);
+}
+__device__ __forceinline__ uint32_t ld_win(const uint8_t *aligned_base, int lane) {
+  return __ldg(reinterpret_cast<const uint32_t *>(aligned_base) + lane);
 }
 
 struct Warp {
@@ -243,7 +267,7 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
   return x;
 }
 
-template <int NB>
+template <int NB, bool FUSED>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kernel(const Params p) {
   __shared__ Smem<NB> sm;
   extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
@@ -285,29 +309,111 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
   // arbiter's priority order, so an id reserved early by a slow warp would
   // become the kernel's tail.
   const uint32_t first_wave = gridDim.x * kWarpsPerBlock;
-  auto issue_task = [&](uint32_t t, int buf) {
-    if (t < p.n_tasks && lane < (int)(sizeof(TaskRec) / 16))
-      cp_async16(rec32 + buf * sizeof(TaskRec) + 16 * lane,
-                 reinterpret_cast<const char *>(&p.tasks[t]) + 16 * lane);
-    cp_commit();
+  auto issue_task = [&](uint32_t t, int buf) {  // prebuilt records: cp.async into shared memory
+    if constexpr (!FUSED) {
+      if (t < p.n_tasks && lane < (int)(sizeof(TaskRec) / 16))
+        cp_async16(rec32 + buf * sizeof(TaskRec) + 16 * lane,
+                   reinterpret_cast<const char *>(&p.tasks[t]) + 16 * lane);
+      cp_commit();
+    }
+  };
+  // fused a1: lane l holds word l & 7 of the task head (hw) and the task's raw
+  // record windows (states and series of point t, series of point t-1); both are
+  // loaded one block before the task starts, so their latency hides behind it
+  uint32_t hw = 0, pf_st = 0, pf_se = 0, pf_pr = 0;
+  auto load_head = [&](uint32_t t) {
+    if constexpr (FUSED) hw = t < p.n_tasks ? __ldg(reinterpret_cast<const uint32_t *>(&p.heads[t]) + (lane & 7)) : 0u;
+  };
+  auto load_windows = [&]() {
+    if constexpr (FUSED) {
+      const uint32_t rec = __shfl_sync(kFull, hw, 2), rec_prev = __shfl_sync(kFull, hw, 3);
+      const uint32_t flags = __shfl_sync(kFull, hw, 5);
+      pf_st = (flags & kHeadLast) ? 0u : ld_win(p.recs + (rec & ~3u), lane);
+      pf_se = (flags & kHeadLast) ? 0u : ld_win(p.recs + ((rec + 64) & ~3u), lane);
+      pf_pr = (flags & kHeadFirst) ? 0u : ld_win(p.recs + ((rec_prev + 64) & ~3u), lane);
+    }
   };
   uint32_t t = blockIdx.x * kWarpsPerBlock + warp;
   int buf = 0;
-  if (t < p.n_tasks) issue_task(t, 0);
+  if (t < p.n_tasks) {
+    issue_task(t, 0);
+    load_head(t);
+    load_windows();
+  }
   while (t < p.n_tasks) {
     cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
-    const TaskRec &r = sm.rec[warp][buf];
-    const int32_t start_group = r.start_group;
-    const uint64_t lo = r.commit_lo, whi = r.write_hi;
-    const int64_t end_cursor = r.end_cursor;
-    const uint32_t task_id = r.task_id;
-    const uint32_t lw = r.lanes[lane];
-    const uint32_t state = r.finals_idx == kNoFinals ? (lw & 0xFFFFu) : p.finals[r.finals_idx * 32 + lane];
-    const int32_t init_group = start_group - (int32_t)(lw >> 16);
-    const int cursor0 = (int)r.cursor0;
-    __syncwarp();
-    // next task: 0 = not asked, 1 = atomic in flight, 2 = record prefetch issued
+    int32_t start_group, init_group, cursor0;
+    uint64_t lo, whi;
+    int64_t end_cursor;
+    uint32_t task_id, state;
+    if constexpr (FUSED) {
+      // a1 in the kernel: expand the split records of points t and t-1 (P:380-394,
+      // tab:metadata_codec): anchor state and group of every lane, the sync starts
+      // (min anchor index) that bound this task's committed range (reading Z13)
+      cursor0 = (int32_t)__shfl_sync(kFull, hw, 0);
+      start_group = (int32_t)__shfl_sync(kFull, hw, 1);
+      const uint32_t rec = __shfl_sync(kFull, hw, 2), rec_prev = __shfl_sync(kFull, hw, 3);
+      const uint32_t maxg_prev = __shfl_sync(kFull, hw, 4), flags = __shfl_sync(kFull, hw, 5);
+      task_id = __shfl_sync(kFull, hw, 6);
+      const int32_t hend = (int32_t)__shfl_sync(kFull, hw, 7);
+      const uint64_t N = ((uint64_t)p.N_hi << 32) | p.N_lo;
+      bool bad_meta = false;
+      int64_t ss_t;
+      if (flags & kHeadLast) {
+        state = p.finals[lane];
+        init_group = start_group - ((uint64_t)start_group * 32 + lane < N ? 0 : 1);
+        ss_t = (int64_t)N;
+        whi = (N + 15) & ~15ull;
+      } else {
+        state = window_u32(pf_st, (rec & 3u) + 2 * lane) & 0xFFFFu;  // states as-is
+        uint32_t w;
+        const uint32_t d = series_elem(pf_se, (rec + 64) & 3u, lane, &w);  // anchor - group
+        bad_meta |= d > (uint32_t)start_group;
+        init_group = start_group - (int32_t)d;
+        int32_t idx = init_group * 32 + lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
+        ss_t = idx;
+        whi = (uint64_t)(ss_t / 32 + 1) * 32;
+      }
+      if (flags & kHeadFirst) {
+        lo = 0;
+        end_cursor = hend;
+      } else {
+        uint32_t w;
+        const uint32_t d = series_elem(pf_pr, (rec_prev + 64) & 3u, lane, &w);
+        bad_meta |= d > maxg_prev;
+        int32_t idx = ((int32_t)maxg_prev - (int32_t)d) * 32 + lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
+        lo = (uint64_t)idx;
+        end_cursor = kNoEndCheck;
+        bad_meta |= (int64_t)lo >= ss_t;  // sync starts strictly increasing
+      }
+      if (__any_sync(kFull, bad_meta)) {  // inconsistent metadata: flag it, skip the task
+        if (lane == 0) {
+          atomicOr(&p.status->flags, 4u);
+          atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
+        }
+        lo = 0;
+        start_group = -1;
+      }
+    } else {
+      const TaskRec &r = sm.rec[warp][buf];
+      start_group = r.start_group;
+      lo = r.commit_lo;
+      whi = r.write_hi;
+      end_cursor = r.end_cursor;
+      task_id = r.task_id;
+      const uint32_t lw = r.lanes[lane];
+      state = r.finals_idx == kNoFinals ? (lw & 0xFFFFu) : p.finals[r.finals_idx * 32 + lane];
+      init_group = start_group - (int32_t)(lw >> 16);
+      cursor0 = (int)r.cursor0;
+      __syncwarp();
+    }
+    // next task: 0 = not asked, 1 = atomic in flight, 2 = record / head in flight,
+    // 3 = (fused) record windows in flight
     int next_state = 0;
     uint32_t t_after = 0, t_next = p.n_tasks;
     auto next_task_step = [&]() {
@@ -317,7 +423,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
       } else if (next_state == 1) {
         t_next = __shfl_sync(kFull, t_after, 0);
         issue_task(t_next, buf ^ 1);
+        load_head(t_next);
         next_state = 2;
+      } else if (next_state == 2) {
+        load_windows();
+        next_state = 3;
       }
     };
 
@@ -377,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
         w.flush(out_blo, 0, woff, wend);
       }
     }
-    while (next_state < 2) next_task_step();
+    while (next_state < 3) next_task_step();
     if (end_cursor != kNoEndCheck) {
       // the task reached its codec's first symbol: the outputs emitted before
       // group 0 (Eq. 3 with f(s_0) 2^(32-n) <= L, i.e. n = 16 and f = 1) are read last
@@ -406,24 +516,43 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
 }
 
 using KernelFn = void (*)(const Params);
-static KernelFn kernel_for(uint32_t nbits) {
+static KernelFn kernel_for(uint32_t nbits, bool fused) {
+  if (fused) switch (nbits) {
+    case 1: return recoil_decode_kernel<1, true>;
+    case 2: return recoil_decode_kernel<2, true>;
+    case 3: return recoil_decode_kernel<3, true>;
+    case 4: return recoil_decode_kernel<4, true>;
+    case 5: return recoil_decode_kernel<5, true>;
+    case 6: return recoil_decode_kernel<6, true>;
+    case 7: return recoil_decode_kernel<7, true>;
+    case 8: return recoil_decode_kernel<8, true>;
+    case 9: return recoil_decode_kernel<9, true>;
+    case 10: return recoil_decode_kernel<10, true>;
+    case 11: return recoil_decode_kernel<11, true>;
+    case 12: return recoil_decode_kernel<12, true>;
+    case 13: return recoil_decode_kernel<13, true>;
+    case 14: return recoil_decode_kernel<14, true>;
+    case 15: return recoil_decode_kernel<15, true>;
+    case 16: return recoil_decode_kernel<16, true>;
+    default: return nullptr;
+  }
   switch (nbits) {
-    case 1: return recoil_decode_kernel<1>;
-    case 2: return recoil_decode_kernel<2>;
-    case 3: return recoil_decode_kernel<3>;
-    case 4: return recoil_decode_kernel<4>;
-    case 5: return recoil_decode_kernel<5>;
-    case 6: return recoil_decode_kernel<6>;
-    case 7: return recoil_decode_kernel<7>;
-    case 8: return recoil_decode_kernel<8>;
-    case 9: return recoil_decode_kernel<9>;
-    case 10: return recoil_decode_kernel<10>;
-    case 11: return recoil_decode_kernel<11>;
-    case 12: return recoil_decode_kernel<12>;
-    case 13: return recoil_decode_kernel<13>;
-    case 14: return recoil_decode_kernel<14>;
-    case 15: return recoil_decode_kernel<15>;
-    case 16: return recoil_decode_kernel<16>;
+    case 1: return recoil_decode_kernel<1, false>;
+    case 2: return recoil_decode_kernel<2, false>;
+    case 3: return recoil_decode_kernel<3, false>;
+    case 4: return recoil_decode_kernel<4, false>;
+    case 5: return recoil_decode_kernel<5, false>;
+    case 6: return recoil_decode_kernel<6, false>;
+    case 7: return recoil_decode_kernel<7, false>;
+    case 8: return recoil_decode_kernel<8, false>;
+    case 9: return recoil_decode_kernel<9, false>;
+    case 10: return recoil_decode_kernel<10, false>;
+    case 11: return recoil_decode_kernel<11, false>;
+    case 12: return recoil_decode_kernel<12, false>;
+    case 13: return recoil_decode_kernel<13, false>;
+    case 14: return recoil_decode_kernel<14, false>;
+    case 15: return recoil_decode_kernel<15, false>;
+    case 16: return recoil_decode_kernel<16, false>;
     default: return nullptr;
   }
 }
@@ -441,8 +570,8 @@ static int configure(dev::KernelFn fn, uint32_t nbits) {
   return (e1 == cudaSuccess && e2 == cudaSuccess) ? RECOIL_OK : RECOIL_E_CUDA;
 }
 
-static int occupancy(uint32_t nbits, int *blocks_per_sm) {
-  dev::KernelFn fn = dev::kernel_for(nbits);
+static int occupancy(uint32_t nbits, bool fused, int *blocks_per_sm) {
+  dev::KernelFn fn = dev::kernel_for(nbits, fused);
   if (!fn) return RECOIL_E_ARG;
   int rc = configure(fn, nbits);
   if (rc) return rc;
@@ -472,6 +601,12 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   if (!d->tasks.empty() && cudaMemcpyAsync(ws + d->tasks_off, d->tasks.data(), sizeof(TaskRec) * d->tasks.size(),
                                            cudaMemcpyHostToDevice, s) != cudaSuccess)
     return RECOIL_E_CUDA;
+  if (!d->heads.empty() && cudaMemcpyAsync(ws + d->tasks_off, d->heads.data(), sizeof(TaskHead) * d->heads.size(),
+                                           cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (d->rec_len && cudaMemcpyAsync(ws + d->rec_off, d->c->bytes + d->rec_src, d->rec_len, cudaMemcpyHostToDevice,
+                                    s) != cudaSuccess)
+    return RECOIL_E_CUDA;
   uint64_t have = d->c->B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c->B - p.word_lo) : 0;
   if (have && cudaMemcpyAsync(d_words, d->c->words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
                   cudaSuccess)
@@ -498,7 +633,7 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
                : RECOIL_E_CUDA;
   }
   if (d->blocks_per_sm == 0) {
-    int rc = occupancy(pl.prob_bits, &d->blocks_per_sm);
+    int rc = occupancy(pl.prob_bits, d->fused, &d->blocks_per_sm);
     if (rc) return rc;
     int dev_id = 0;
     if (cudaGetDevice(&dev_id) != cudaSuccess ||
@@ -510,6 +645,11 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
   prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
   prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
   prm.tasks = reinterpret_cast<const TaskRec *>(ws + d->tasks_off);
+  prm.heads = reinterpret_cast<const TaskHead *>(ws + d->tasks_off);
+  prm.recs = reinterpret_cast<const uint8_t *>(ws + d->rec_off);
+  prm.N_lo = (uint32_t)d->c->N;
+  prm.N_hi = (uint32_t)(d->c->N >> 32);
+  prm.G = (int32_t)d->c->G;
   prm.status = reinterpret_cast<DeviceStatus *>(ws);
   prm.words = d_words;
   prm.out = d_out;
@@ -520,7 +660,7 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
   prm.k4096 = 4096;
   const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
-  dev::kernel_for(pl.prob_bits)<<<grid, dev::kThreads, smem_bytes(pl.prob_bits), s>>>(prm);
+  dev::kernel_for(pl.prob_bits, d->fused)<<<grid, dev::kThreads, smem_bytes(pl.prob_bits), s>>>(prm);
   return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
 }
 
@@ -531,6 +671,7 @@ extern "C" int recoil_decoder_status(recoil_decoder *dec, const void *d_workspac
   if (cudaMemcpyAsync(&st, d_workspace, sizeof(st), cudaMemcpyDeviceToHost, s) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return RECOIL_E_CUDA;
   if (bad) *bad = st.bad_task ? (uint64_t)(0xFFFFFFFFu - st.bad_task) : UINT64_MAX;
+  if (st.flags & 4u) return RECOIL_E_INCONSISTENT;
   if (st.flags & 1u) return RECOIL_E_UNDERFLOW;
   if (st.flags & 2u) return RECOIL_E_SYNC;
   return RECOIL_OK;
@@ -548,7 +689,7 @@ extern "C" int recoil_decode_occupancy(int device, uint32_t nbits, int *warps_pe
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0;
-  int rc = occupancy(nbits, &per_sm);
+  int rc = occupancy(nbits, true, &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;

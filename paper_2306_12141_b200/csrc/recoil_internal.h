@@ -31,13 +31,18 @@ struct Container {
   std::vector<uint64_t> maxg;     // Recoil: M-1 anchor (max) group IDs
   std::vector<uint16_t> state;    // Recoil: (M-1) x W anchor states (< L)
   std::vector<uint16_t> gdiff;    // Recoil: (M-1) x W group differences to the anchor
-  std::vector<int64_t> sync_start, bidx;  // Recoil: per point min / max anchor index (filled by parse)
+  std::vector<int64_t> sync_start, bidx;  // Recoil: per point min / max anchor index (full parse)
+  bool light = false;             // Recoil light parse: state/gdiff/sync_start/bidx left empty
+  std::vector<uint64_t> rec_off;  // Recoil: container byte offset of each split record (P + 1 entries)
+  const uint8_t *bytes = nullptr; // the container
   std::vector<uint64_t> part_words; // partitioned: M word counts
   const uint8_t *words = nullptr; // B little-endian u16
   uint64_t header_bytes = 0, meta_bytes = 0, total_bytes = 0;
 };
 
-int parse_container(const uint8_t *c, uint64_t len, Container *out);
+int parse_container(const uint8_t *c, uint64_t len, Container *out, bool light = false);
+// Light parse helper: sync start and boundary index of split point k (decodes one record).
+int point_span_light(const Container &c, uint64_t k, int64_t *sync_start, int64_t *bidx);
 // Serialise a Recoil container (offset/maxg/state/gdiff/finals/f from `c`,
 // words from `words` (B little-endian u16 bytes)).  out == nullptr: size only.
 int write_recoil_container(const Container &c, const uint8_t *words, uint8_t *out, uint64_t *len);
@@ -65,8 +70,25 @@ struct alignas(16) TaskRec {
 };
 static_assert(sizeof(TaskRec) == 192, "TaskRec layout");
 
+// Fused-a1 task header (Recoil containers on the GPU, DESIGN.md row a1): the
+// O(M) sequential part of the metadata (global series, record offsets) is
+// decoded on the host; the kernel expands the O(M W) per-lane part (anchor
+// states and group differences) from the raw records itself.
+struct alignas(16) TaskHead {
+  int32_t cursor0;      // slice-relative first word (offset of point t; B - 1 for the last task)
+  int32_t start_group;  // anchor group of point t (G - 1 for the last task)
+  uint32_t rec;         // byte offset of point t's record in the device record area
+  uint32_t rec_prev;    // byte offset of point t-1's record
+  uint32_t maxg_prev;   // anchor group of point t-1
+  uint32_t flags;       // kHeadLast: entered from the final states; kHeadFirst: t == 0
+  uint32_t task_id;
+  int32_t end_cursor;   // t == 0: slice-relative end cursor (-1 - word_lo)
+};
+static_assert(sizeof(TaskHead) == 32, "TaskHead layout");
+constexpr uint32_t kHeadLast = 1, kHeadFirst = 2;
+
 struct DeviceStatus {   // first 16 B of the workspace, zeroed before every decode
-  uint32_t flags;       // bit 0 underflow, bit 1 end-state mismatch
+  uint32_t flags;       // bit 0 underflow, bit 1 end-state mismatch, bit 2 inconsistent metadata
   uint32_t bad_task;    // atomicMax of (0xFFFFFFFF - failing task id); 0 = none
   uint32_t next_task;   // persistent-warp task counter
   uint32_t pad;
@@ -79,8 +101,12 @@ struct Decoder {
   std::vector<uint8_t> lut;        // n <= 12: 2^n packed u32 s | bias << 8 | f << 20;
                                    // n >= 13: 2^n symbol bytes + 256 x u32 (f | F << 16)
   std::vector<uint32_t> finals;    // K x 32 u32 states referenced by finals_idx
-  std::vector<TaskRec> tasks;
-  uint64_t lut_off = 0, finals_off = 0, tasks_off = 0;  // workspace byte offsets
+  std::vector<TaskRec> tasks;      // prebuilt records (partitioned containers, CPU decoder)
+  bool fused = false;              // Recoil on the GPU: heads + raw records, expanded in-kernel
+  std::vector<TaskHead> heads;
+  uint64_t rec_src = 0, rec_len = 0;  // container byte span of the records the plan needs
+  uint64_t lut_off = 0, finals_off = 0, tasks_off = 0, rec_off = 0;  // workspace byte offsets
+  uint32_t n_tasks = 0;
   int single_symbol = -1;          // >= 0: the model has one symbol (f = 2^n): decode = fill
   int blocks_per_sm = 0, sm_count = 0;  // launch geometry (occupancy API), cached
 };
