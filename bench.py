@@ -371,11 +371,18 @@ def main():
                "sample": desc, "seconds": round(dt, 3)}
         t0 = time.perf_counter()
         threads = os.cpu_count() or 1
-        out_cpu = R.recoil_decode_cpu(cont, threads)
+        out_cpu = R.recoil_decode_cpu_ex(cont, threads, R.RECOIL_CPU_SCALAR)
         dt_mt = time.perf_counter() - t0
         extra["cpu_mt_library"] = {"value": round(N_total / dt_mt / 1e9, 4), "unit": "GB/s", "threads": threads,
                                    "bit_exact": bool((out_cpu == sym).all()),
-                                   "note": "recoil_decode_cpu: scalar MT host decoder (baseline, not a fallback)"}
+                                   "note": "recoil_decode_cpu_ex(SCALAR): scalar MT host decoder (baseline, not a fallback)"}
+        if R.recoil_cpu_simd():
+            t0 = time.perf_counter()
+            out_cpu = R.recoil_decode_cpu_ex(cont, threads, 0)
+            dt_mt = time.perf_counter() - t0
+            extra["cpu_mt_avx512"] = {"value": round(N_total / dt_mt / 1e9, 4), "unit": "GB/s", "threads": threads,
+                                      "bit_exact": bool((out_cpu == sym).all()),
+                                      "note": "recoil_decode_cpu: AVX-512 MT host decoder (NEXT row 3; baseline)"}
 
     prof = {}
     pf = os.path.join(ROOT, "profiles", "ncu_traffic.json")

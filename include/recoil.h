@@ -235,9 +235,17 @@ int recoil_shard_plan(const uint8_t *container, uint64_t len, uint32_t n_shards,
 /* ---------------------------------------------------------------------- */
 
 /* Multithreaded CPU Recoil / partitioned decoder: one task per split, up to
- * `threads` threads (0 = hardware concurrency), scalar code.  out: N bytes.
+ * `threads` threads (0 = hardware concurrency); AVX-512 task decoder when the
+ * CPU has AVX-512 F/BW/VL/VBMI2 (P:429's AVX-512 decoder: 16 lanes per
+ * instruction, two vectors per 32-lane group), else scalar.  out: N bytes.
  * Errors: container errors, E_UNDERFLOW, E_SYNC. */
 int recoil_decode_cpu(const uint8_t *container, uint64_t len, uint8_t *out, uint32_t threads);
+
+#define RECOIL_CPU_SCALAR 1u /* recoil_decode_cpu_ex flag: force the scalar task decoder */
+int recoil_decode_cpu_ex(const uint8_t *container, uint64_t len, uint8_t *out, uint32_t threads, uint32_t flags);
+
+/* 1 if recoil_decode_cpu uses the AVX-512 task decoder on this CPU, else 0. */
+int recoil_cpu_simd(void);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ EXPORTS = [
     "recoil_strerror", "recoil_build_model", "recoil_encode", "recoil_combine_splits", "recoil_inspect",
     "recoil_partitioned_encode", "recoil_decoder_create", "recoil_decoder_plan", "recoil_decoder_upload",
     "recoil_decode", "recoil_decoder_status", "recoil_decoder_launches", "recoil_decoder_destroy",
-    "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu",
+    "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu", "recoil_decode_cpu_ex", "recoil_cpu_simd",
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
     "recoil_pipeline_launches", "recoil_pipeline_destroy",
 ]
@@ -91,6 +91,8 @@ def load(path: str = LIB_PATH):
         "recoil_decode_occupancy": (i32, [i32, u32, P, P]),
         "recoil_shard_plan": (i32, [P, u64, u32, P]),
         "recoil_decode_cpu": (i32, [P, u64, P, u32]),
+        "recoil_decode_cpu_ex": (i32, [P, u64, P, u32, u32]),
+        "recoil_cpu_simd": (i32, []),
         "recoil_pipeline_create": (i32, [P, u64, u64, u64, u32, P]),
         "recoil_pipeline_device_bytes": (i32, [P, u32, P]),
         "recoil_pipeline_run": (i32, [P, P, P, P, u32]),
@@ -188,6 +190,22 @@ def recoil_decode_cpu(container, threads: int = 0, out: np.ndarray | None = None
         out = np.empty(N, dtype=np.uint8)
     _check(load().recoil_decode_cpu(c.ctypes.data, c.size, _ptr(out), threads), "recoil_decode_cpu")
     return out
+
+
+RECOIL_CPU_SCALAR = 1
+
+
+def recoil_decode_cpu_ex(container, threads: int = 0, flags: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    c = _u8(container)
+    N = recoil_inspect(c)["n_symbols"]
+    if out is None:
+        out = np.empty(N, dtype=np.uint8)
+    _check(load().recoil_decode_cpu_ex(c.ctypes.data, c.size, _ptr(out), threads, flags), "recoil_decode_cpu_ex")
+    return out
+
+
+def recoil_cpu_simd() -> bool:
+    return bool(load().recoil_cpu_simd())
 
 
 def recoil_decode_occupancy(device: int, prob_bits: int) -> tuple[int, int]:

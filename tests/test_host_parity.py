@@ -205,3 +205,57 @@ def test_decoder_plan_layout():
     p16 = R.recoil_decoder_plan(h)
     assert p16["prob_bits"] == 16 and p16["workspace_bytes"] >= (1 << 16) + 1024
     R.recoil_decoder_destroy(h)
+
+
+@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX-512 F/BW/VL/VBMI2")
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_avx512_cpu_decoder_matches_scalar_and_input(n):
+    """NEXT row 3: the AVX-512 task decoder (expand-load refill + LUT gathers) equals the
+    scalar decoder and the input, for every n (packed LUT n <= 12, split tables above)."""
+    kind = ("exp", "text", "image")[n % 3]
+    sym = synth.workload(kind, 400_001 + 37 * n, seed=100 + n, lam=50)
+    hist = synth.histogram(sym)
+    if (hist > 0).sum() > (1 << n):
+        sym = (sym % (1 << min(n, 8))).astype(np.uint8)
+        hist = synth.histogram(sym)
+    f = oracle.build_model(hist, n)
+    for M in (1, 7, 333):
+        c = R.recoil_encode(sym, f, n, M)
+        a = R.recoil_decode_cpu_ex(c, 4, 0)
+        b = R.recoil_decode_cpu_ex(c, 4, R.RECOIL_CPU_SCALAR)
+        assert (a == sym).all() and (b == sym).all()
+    p = R.recoil_partitioned_encode(sym, f, n, 13)
+    assert (R.recoil_decode_cpu_ex(p, 3, 0) == sym).all()
+
+
+@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX-512 F/BW/VL/VBMI2")
+def test_avx512_cpu_decoder_edges_and_corruption():
+    rng = np.random.default_rng(8)
+    hist = np.zeros(256, dtype=np.uint64)
+    hist[:200] = rng.integers(1, 5, size=200)
+    hist[7] = 10 ** 7
+    f = oracle.build_model(hist, 16)
+    rare = [s for s in range(256) if f[s] == 1]
+    sym = synth.table_bytes(50000, (f / f.sum()).tolist(), 4)
+    sym[:32] = rare[0]  # n = 16 emissions before group 0
+    for c in (R.recoil_encode(sym, f, 16, 5), R.recoil_partitioned_encode(sym, f, 16, 7)):
+        assert (R.recoil_decode_cpu_ex(c, 2, 0) == sym).all()
+    for N in (0, 1, 31, 32, 33, 95):  # empty / ragged groups
+        s = synth.text_bytes(N, N)
+        ff = oracle.build_model(synth.histogram(s) if N else np.ones(256, dtype=np.uint64), 11)
+        assert (R.recoil_decode_cpu_ex(R.recoil_encode(s, ff, 11, 3), 1, 0) == s).all()
+    s = synth.text_bytes(300000, 9)
+    ff = oracle.build_model(synth.histogram(s), 11)
+    c = R.recoil_encode(s, ff, 11, 16)
+    info = R.recoil_inspect(c)
+    bad = c.copy()
+    hdr = len(c) - 2 * info["n_words"]
+    bad[hdr + 2 * (info["n_words"] // 2)] ^= 0x5A  # flip a bitstream word
+    errs = []
+    for flags in (0, R.RECOIL_CPU_SCALAR):
+        try:
+            out = R.recoil_decode_cpu_ex(bad, 2, flags)
+            errs.append(("ok", int((out != s).sum() > 0)))
+        except R.RecoilError as e:
+            errs.append(("err", e.rc))
+    assert errs[0] == errs[1]  # same verdict from both decoders
