@@ -194,7 +194,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
-    ap.add_argument("--waves", type=int, default=2, help="splits per GPU = waves x resident warps")
+    ap.add_argument("--waves", type=int, default=1, help="splits per GPU = waves x resident warps (1: one split per resident warp, the decoder-adaptive choice of P:84)")
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
     ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
     ap.add_argument("--chunks", type=int, default=8, help="e2e pipeline chunks per GPU")

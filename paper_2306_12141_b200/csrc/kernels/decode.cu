@@ -38,10 +38,16 @@ namespace dev {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
+// Resident blocks per SM the kernel is compiled for.  The steady state is bound
+// by the latency of its per-group dependency chain, so more warps help: n <= 11
+// runs 6 blocks (48 warps, 40 registers; 7 blocks at 32 registers measured
+// 11 % slower, 5 blocks 6 % slower); n = 12 (16 KB LUT) and n >= 13 (up to
+// 64 KB symbol table) are shared-memory limited and keep 48 registers.
 #ifndef RECOIL_MIN_BLOCKS
-#define RECOIL_MIN_BLOCKS 5
+#define RECOIL_MIN_BLOCKS 6
 #endif
-constexpr int kMinBlocksPerSM = RECOIL_MIN_BLOCKS;  // 5: 40 resident warps/SM (<= 48 registers); 48 warps measured slower
+template <int NB>
+constexpr int min_blocks() { return NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
 constexpr int kRingChunks = 4;
 constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
 constexpr uint32_t kRingBytes = 2 * kRingWords;
@@ -64,7 +70,7 @@ struct Params {
   // Runtime constants, opaque to ptxas, that keep some steady-state work on the
   // FMA pipe (IMAD) instead of the ALU pipe, which is the busiest one:
   int32_t neg2;           // -2: cursor arithmetic as IMAD instead of IADD3
-  uint32_t k4096;         // 2^12: bias = (e * 2^12) >> 20 as IMAD + SHF instead of SHF + LOP3
+  int32_t kneg4096;       // -2^12: see Warp::decode
 };
 
 // Static shared memory per block (about 33 KB for n = 11): the word rings need
@@ -72,15 +78,20 @@ struct Params {
 constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 template <int NB>
 struct __align__(16) Smem {
-  // 8 x 2 KB word windows + 2 KB so the first can start 2 KB-aligned: the
-  // shared window does not honour more than 1 KB alignment of static data
-  uint16_t ring[kWarpsPerBlock + 1][kRingWords];
+  // Order matters: the CTA's static shared memory starts 1 KB into its shared
+  // window (the reserved system area), so stage + rec (7 KB) put the LUT on an
+  // 8 KB boundary, and a LUT of <= 8 KB (n <= 11) is addressed with one LOP3:
+  // base | ((x << 2) & mask).  The LUT is at least 2 KB, so the word rings
+  // after it start 2 KB-aligned (ring addresses are base | (pos & 0x7FE)).
+  // Both alignments are checked at kernel start.
   uint8_t stage[kWarpsPerBlock][kBlockBytes];  // 8 x 512 B output staging
   TaskRec rec[kWarpsPerBlock][2];              // current / next task record
   // n <= 12: packed LUT s | bias << 8 | f << 20.  n >= 13 (NEXT row 1):
   // f and F per symbol here, the 2^n slot -> symbol bytes in dynamic smem.
-  uint32_t lut[NB <= kNarrowMaxBits ? (1 << NB) : 256];
+  uint32_t lut[NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512];
+  uint16_t ring[kWarpsPerBlock][kRingWords];   // 8 x 2 KB word windows
 };
+constexpr int kOrLutMaxBits = 11;  // LUT base alignment trick up to 8 KB
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
@@ -142,6 +153,7 @@ struct Warp {
   const Params *p;
   uint32_t ring32;   // 2 KB-aligned shared address of this warp's word ring
   uint32_t stage32;  // this warp's 512-B staging block + lane
+  uint32_t lut32;    // shared address of the packed LUT (n <= 12)
   uint32_t gt;       // lanes above this one
   int lane;
   int cursor2;       // 2 x (slice-relative index of the next word to read)
@@ -154,12 +166,16 @@ struct Warp {
                  p->words + (size_t)c * kChunkWords + lane * 8);
     cp_commit();
   }
-  // Keep chunks cchunk and cchunk-1 complete and cchunk-2 in flight.  8 groups
-  // consume at most 256 words, so one check covers the next 8 groups.
+  // Keep chunks cchunk, cchunk-1, cchunk-2 complete and cchunk-3 in flight (the
+  // 4-chunk ring).  16 groups consume at most 512 words (two chunks), so one
+  // check covers a whole output block.
   __device__ __forceinline__ void window_check() {
-    if ((cursor2 >> 9) != cchunk) {
-      --cchunk;
-      issue_chunk(cchunk - 2);
+    const int c = cursor2 >> 9;
+    if (c != cchunk) {
+      do {
+        --cchunk;
+        issue_chunk(cchunk - 3);
+      } while (cchunk > c);
       cp_wait<1>();
       __syncwarp();
     }
@@ -171,18 +187,21 @@ struct Warp {
     const bool need = x < kL;
     const uint32_t m = __ballot_sync(kFull, need);
     const int pre = __popc(m & gt);
-    const int total = (int)__reduce_add_sync(kFull, (uint32_t)need);
+    const int step2 = __reduce_add_sync(kFull, need ? -2 : 0);  // -2 x (words this group)
     const uint32_t w = lds_u16(ring32 | ((uint32_t)(cursor2 + pre * p->neg2) & (kRingBytes - 2)));
-    cursor2 += total * p->neg2;
+    cursor2 += step2;
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
   template <int NB>
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
     if constexpr (NB <= kNarrowMaxBits) {
-      const uint32_t e = lut[x & ((1u << NB) - 1)];
+      const uint32_t e = NB <= kOrLutMaxBits ? lds_u32(lut32 | ((x << 2) & ((4u << NB) - 4)))
+                                             : lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
       sts_u8(stage32 + k * 32, e);
-      return (e >> 20) * (x >> NB) + ((e * p->k4096) >> 20);  // f (x >> n) + bias
+      // f (x >> n) + bias as f ((x >> n) - 2^12) + (e >> 8), since e >> 8 = bias + 2^12 f
+      // (mod 2^32; the true result is < 2^32): LEA.HI + SHF + SHF + IMAD
+      return (e >> 20) * ((x >> NB) + (uint32_t)p->kneg4096) + (e >> 8);
     } else {
       const uint32_t slot = x & ((1u << NB) - 1);
       const uint32_t s = sym[slot];
@@ -193,6 +212,11 @@ struct Warp {
   }
   // a8: write an output block: every 16-B chunk of this lane inside the task's
   // write window [woff, wend) (offsets relative to the block's base `dst`).
+  __device__ __forceinline__ void flush_at(uint8_t *dst, int c, int woff, int wend) {
+    __syncwarp();
+    if (c >= woff && c + 16 <= wend) stg_v4(dst + 16 * lane, lds_v4(stage32 + 15 * lane));
+    __syncwarp();
+  }
   __device__ __forceinline__ void flush(uint8_t *dst, int rel, int woff, int wend) {
     __syncwarp();
     const int c = rel + 16 * lane;
@@ -232,10 +256,7 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const
     case 11: RECOIL_STEP(11) [[fallthrough]];
     case 10: RECOIL_STEP(10) [[fallthrough]];
     case 9: RECOIL_STEP(9) [[fallthrough]];
-    case 8:
-      RECOIL_STEP(8)
-      w.window_check();  // entered at slot >= 8: re-check before slots 7..0
-      [[fallthrough]];
+    case 8: RECOIL_STEP(8) [[fallthrough]];
     case 7: RECOIL_STEP(7) [[fallthrough]];
     case 6: RECOIL_STEP(6) [[fallthrough]];
     case 5: RECOIL_STEP(5) [[fallthrough]];
@@ -254,13 +275,7 @@ template <int NB>
 __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x) {
   w.window_check();
 #pragma unroll
-  for (int k = 15; k >= 8; --k) {
-    x = w.refill(x);
-    x = w.decode<NB>(lut, sym, x, k);
-  }
-  w.window_check();
-#pragma unroll
-  for (int k = 7; k >= 0; --k) {
+  for (int k = 15; k >= 0; --k) {
     x = w.refill(x);
     x = w.decode<NB>(lut, sym, x, k);
   }
@@ -268,7 +283,7 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
 }
 
 template <int NB, bool FUSED>
-__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kernel(const Params p) {
   __shared__ Smem<NB> sm;
   extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
 
@@ -293,9 +308,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
   w.lane = threadIdx.x & 31;
   const int lane = w.lane;
   const int warp = threadIdx.x >> 5;
-  w.ring32 = ((smem_addr(&sm.ring[0][0]) + kRingBytes - 1) & ~(kRingBytes - 1)) + warp * kRingBytes;
+  w.ring32 = smem_addr(&sm.ring[warp][0]);
   w.stage32 = smem_addr(&sm.stage[warp][lane]);
   w.gt = lanemask_gt();
+  w.lut32 = smem_addr(sm.lut);
+  if ((NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
+    // shared-memory layout assumption broken: fail loudly
+    if (threadIdx.x == 0) atomicOr(&p.status->flags, 4u);
+    return;
+  }
   w.cchunk = 0;
   const uint32_t rec32 = smem_addr(&sm.rec[warp][0]);
   const uint32_t *lut = sm.lut;
@@ -431,12 +452,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
       }
     };
 
-    // a7: word window -- chunks c, c-1 resident, c-2 in flight
+    // a7: word window -- chunks c, c-1, c-2 resident, c-3 in flight
     w.cursor2 = 2 * cursor0;
     w.cchunk = cursor0 >> 8;
     w.issue_chunk(w.cchunk);
     w.issue_chunk(w.cchunk - 1);
     w.issue_chunk(w.cchunk - 2);
+    w.issue_chunk(w.cchunk - 3);
     cp_wait<1>();
     __syncwarp();
 
@@ -474,13 +496,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM) recoil_decode_kerne
     }
     if (g >= lo_group) {
       // whole blocks above the block of lo_group; the next task id is requested
-      // two blocks before the end
+      // three blocks before the end
       int rel = (g >> 4) - b_lo;
       const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      for (; rel >= full_lo; --rel) {
-        if (rel - full_lo < 3) next_task_step();
+      uint8_t *dst = out_blo + rel * (int)kBlockBytes;
+      int c = rel * (int)kBlockBytes + 16 * lane;  // this lane's 16-B chunk, block-relative
+      for (; rel >= full_lo + 3; --rel) {
         x = run_block<NB>(w, lut, sym, x);
-        w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
+        w.flush_at(dst, c, woff, wend);
+        dst -= kBlockBytes;
+        c -= (int)kBlockBytes;
+      }
+      for (; rel >= full_lo; --rel) {
+        next_task_step();
+        x = run_block<NB>(w, lut, sym, x);
+        w.flush_at(dst, c, woff, wend);
+        dst -= kBlockBytes;
+        c -= (int)kBlockBytes;
       }
       if (full_lo) {  // tail: the partial block of lo_group
         x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
@@ -657,7 +689,7 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
   prm.n_chunks = (int32_t)(pl.word_count / kChunkWords);
   prm.n_tasks = pl.n_tasks;
   prm.neg2 = -2;
-  prm.k4096 = 4096;
+  prm.kneg4096 = -4096;
   const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
   dev::kernel_for(pl.prob_bits, d->fused)<<<grid, dev::kThreads, smem_bytes(pl.prob_bits), s>>>(prm);
