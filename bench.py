@@ -162,7 +162,12 @@ def run_reference(args, rank, world):
     from paper_2306_12141_b200 import recoil as R
     sym = make_stream(args.config, world, args.lam)
     f = R.recoil_build_model(np.bincount(sym, minlength=256).astype(np.uint64), 11)
-    M = args.splits or 11840 * world
+    # same split count as our arm: waves x 48 resident warps/SM (the decode kernel's occupancy at n = 11)
+    # x SMs per GPU; the SM count is read from torch, not from our library
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+    waves = args.waves or (1 if args.config == "config2" else 2)
+    M = args.splits or (16 if args.config == "config1" else 48 * sms * waves) * world
     c = R.recoil_encode(sym, f, 11, M)
     M = R.recoil_inspect(c)["n_splits"]
     per_step = max(1, M // 64)  # ~1/64 of the stream per step: bounded sample
@@ -194,7 +199,10 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
-    ap.add_argument("--waves", type=int, default=1, help="splits per GPU = waves x resident warps (1: one split per resident warp, the decoder-adaptive choice of P:84)")
+    ap.add_argument("--waves", type=int, default=0,
+                    help="splits per GPU = waves x resident warps; 0 = per-config default (config2: 1, one split "
+                         "per resident warp, the decoder-adaptive choice of P:84; configs 3/5: 2, measured best for "
+                         "their 10x longer splits)")
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
     ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
     ap.add_argument("--chunks", type=int, default=8, help="e2e pipeline chunks per GPU")
@@ -234,6 +242,8 @@ def main():
     hist = np.bincount(sym, minlength=256).astype(np.uint64)
     f = R.recoil_build_model(hist, 11)
     warps, sms = R.recoil_decode_occupancy(local, 11)
+    if not args.waves:
+        args.waves = 1 if args.config == "config2" else 2
     M_gpu = args.splits or (16 if args.config == "config1" else warps * sms * args.waves)
     if args.config == "config4":
         c_full = R.recoil_encode(sym, f, 11, 65536 * world)

@@ -82,6 +82,13 @@ def _load():
         "or_recoil_decode_tasks": (i32, [P, u64, P, u32, P, P]),
         "or_partitioned_encode": (i32, [P, u64, P, u32, u32, u32, P, P]),
         "or_partitioned_decode": (i32, [P, u64, P]),
+        "or_quantize": (i32, [P, u32, u32, P]),
+        "or_ad_interleaved_encode": (i64, [P, u64, P, u32, P, P, P, u32, u32, P, P, P]),
+        "or_ad_interleaved_decode": (i32, [P, u64, P, u64, P, u32, P, P, P, u32, u32, P]),
+        "or_ad_decode_from": (i32, [P, P, u32, P, P, P, u32, u32, u64, i64, i64, P, P, u64, u64, P]),
+        "or_ad_recoil_encode": (i32, [P, u64, P, u32, P, P, P, u32, u32, u32, P, P]),
+        "or_ad_recoil_decode": (i32, [P, u64, P, P]),
+        "or_ad_recoil_decode_task": (i32, [P, u64, P, u32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -305,3 +312,96 @@ def partitioned_decode(container: bytes) -> np.ndarray:
     out = np.zeros(max(N, 1), dtype=np.uint8)
     _check(_load().or_partitioned_decode(c.ctypes.data, c.size, out.ctypes.data))
     return out[:N]
+
+
+# --- adaptive coding: index-keyed models, 16-bit symbols (P:227 (3)) ---------
+
+def quantize(hist, n: int) -> np.ndarray:
+    """Reading Z19's quantiser over any number of entries (build_model = 256 entries)."""
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.uint64))
+    f = np.zeros(h.size, dtype=np.uint32)
+    _check(_load().or_quantize(h.ctypes.data, h.size, n, f.ctypes.data))
+    return f
+
+
+def _models(models):
+    base = np.ascontiguousarray(np.asarray(models["base"], dtype=np.uint32))
+    ln = np.ascontiguousarray(np.asarray(models["len"], dtype=np.uint32))
+    f = np.ascontiguousarray(np.asarray(models["f"], dtype=np.uint32))
+    assert base.size == ln.size and f.size == int(ln.sum())
+    return base, ln, f
+
+
+def _u16(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint16))
+
+
+def _mid(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+
+
+def ad_interleaved_encode(sym, mid, models, n: int, W: int = 32):
+    """-> (words u16[B], final u32[W], events)"""
+    s, m = _u16(sym), _mid(mid)
+    base, ln, f = _models(models)
+    N = s.size
+    words = np.zeros(4 * N + 8, dtype=np.uint16)
+    final = np.zeros(W, dtype=np.uint32)
+    ev = np.zeros(4 * N + 8, dtype=EVENT_DTYPE)
+    B = _check(_load().or_ad_interleaved_encode(_ptr(s), N, _ptr(m), base.size, base.ctypes.data, ln.ctypes.data,
+                                                f.ctypes.data, n, W, words.ctypes.data, final.ctypes.data,
+                                                ev.ctypes.data))
+    return words[:B].copy(), final, ev[:B].copy()
+
+
+def ad_interleaved_decode(words, final, N: int, mid, models, n: int, W: int = 32) -> np.ndarray:
+    w = _u16(words)
+    fin = np.ascontiguousarray(np.asarray(final, dtype=np.uint32))
+    m = _mid(mid)
+    base, ln, f = _models(models)
+    out = np.zeros(max(N, 1), dtype=np.uint16)
+    _check(_load().or_ad_interleaved_decode(_ptr(w), w.size, fin.ctypes.data, N, _ptr(m), base.size, base.ctypes.data,
+                                            ln.ctypes.data, f.ctypes.data, n, W, out.ctypes.data))
+    return out[:N]
+
+
+def ad_decode_from(words, mid, models, n: int, W: int, N: int, cursor0: int, start_group: int, init_state,
+                   init_group, commit_lo: int, commit_hi: int):
+    w = _u16(words)
+    m = _mid(mid)
+    base, ln, f = _models(models)
+    st = np.ascontiguousarray(np.asarray(init_state, dtype=np.uint32))
+    ig = np.ascontiguousarray(np.asarray(init_group, dtype=np.int64))
+    out = np.zeros(max(N, 1), dtype=np.uint16)
+    rc = _load().or_ad_decode_from(_ptr(w), _ptr(m), base.size, base.ctypes.data, ln.ctypes.data, f.ctypes.data, n, W,
+                                   N, cursor0, start_group, st.ctypes.data, ig.ctypes.data, commit_lo, commit_hi,
+                                   out.ctypes.data)
+    return rc, out[:N]
+
+
+def ad_recoil_encode(sym, mid, models, n: int, M: int, W: int = 32) -> bytes:
+    s, m = _u16(sym), _mid(mid)
+    base, ln, f = _models(models)
+    return _sized_call(_load().or_ad_recoil_encode, _ptr(s), s.size, _ptr(m), base.size, base.ctypes.data,
+                       ln.ctypes.data, f.ctypes.data, n, W, M)
+
+
+def ad_recoil_decode(container: bytes, mid) -> np.ndarray:
+    c = _u8(container)
+    m = _mid(mid)
+    N = container_info(container)["N"]
+    out = np.zeros(max(N, 1), dtype=np.uint16)
+    _check(_load().or_ad_recoil_decode(c.ctypes.data, c.size, _ptr(m), out.ctypes.data))
+    return out[:N]
+
+
+def ad_recoil_decode_task(container: bytes, mid, task: int, out: np.ndarray | None = None):
+    c = _u8(container)
+    m = _mid(mid)
+    N = container_info(container)["N"]
+    if out is None:
+        out = np.zeros(max(N, 1), dtype=np.uint16)
+    lo, hi = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(_load().or_ad_recoil_decode_task(c.ctypes.data, c.size, _ptr(m), task, out.ctypes.data,
+                                            ctypes.byref(lo), ctypes.byref(hi)))
+    return out, lo.value, hi.value

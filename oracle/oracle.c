@@ -26,25 +26,30 @@ static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 /* Floor of hist*2^n/total, every present symbol at least 1, then the
  * shortfall handed out by largest remainder (ties: smaller symbol); an
  * excess (caused by the min-1 rule) is taken from the largest f (ties:
- * smaller count, then smaller symbol). */
-int or_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]) {
-  if (n < 1 || n > 16) return OR_E_ARG;
+ * smaller count, then smaller symbol).  `count` entries (256 for bytes; a
+ * model of the adaptive codec may have up to 2^16). */
+int or_quantize(const uint64_t *hist, uint32_t count, uint32_t n, uint32_t *f) {
+  if (n < 1 || n > 16 || count < 1) return OR_E_ARG;
   uint64_t total = 0, distinct = 0, R = 1ull << n;
-  for (int s = 0; s < 256; ++s) {
+  for (uint32_t s = 0; s < count; ++s) {
     total += hist[s];
     if (hist[s]) distinct++;
   }
   if (total == 0 || distinct > R) return OR_E_MODEL;
-  uint64_t rem[256], sum = 0;
-  int given[256] = {0};
-  for (int s = 0; s < 256; ++s) {
+  uint64_t *rem = (uint64_t *)calloc(count, sizeof(uint64_t));
+  int *given = (int *)calloc(count, sizeof(int));
+  if (!rem || !given) { free(rem); free(given); return OR_E_NOMEM; }
+  uint64_t sum = 0;
+  for (uint32_t s = 0; s < count; ++s) {
     if (!hist[s]) {
       f[s] = 0;
       rem[s] = 0;
       continue;
     }
-    uint64_t q = hist[s] * R / total;
-    rem[s] = hist[s] * R % total;
+    /* hist * R may exceed 64 bits for large counts: 128-bit product */
+    unsigned __int128 prod = (unsigned __int128)hist[s] * R;
+    uint64_t q = (uint64_t)(prod / total);
+    rem[s] = (uint64_t)(prod % total);
     f[s] = (uint32_t)(q < 1 ? 1 : q);
     if (q < 1) given[s] = 1; /* raised to 1: already rounded up */
     sum += f[s];
@@ -52,22 +57,28 @@ int or_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]) {
   /* largest remainder: the shortfall is < the number of symbols not raised
    * to 1, so each gets at most one extra count */
   while (sum < R) {
-    int best = -1;
-    for (int s = 0; s < 256; ++s)
+    int64_t best = -1;
+    for (uint32_t s = 0; s < count; ++s)
       if (hist[s] && !given[s] && (best < 0 || rem[s] > rem[best])) best = s;
-    if (best < 0) return OR_E_MODEL; /* unreachable */
+    if (best < 0) { free(rem); free(given); return OR_E_MODEL; } /* unreachable */
     given[best] = 1;
     f[best]++;
     sum++;
   }
   while (sum > R) { /* largest f first; ties: smaller count, then smaller symbol */
-    int best = -1;
-    for (int s = 0; s < 256; ++s)
+    int64_t best = -1;
+    for (uint32_t s = 0; s < count; ++s)
       if (f[s] > 1 && (best < 0 || f[s] > f[best] || (f[s] == f[best] && hist[s] < hist[best]))) best = s;
     f[best]--;
     sum--;
   }
+  free(rem);
+  free(given);
   return OR_OK;
+}
+
+int or_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]) {
+  return or_quantize(hist, 256, n, f);
 }
 
 static void cdf_of(const uint32_t f[256], uint32_t F[256]) {
@@ -450,7 +461,10 @@ static uint64_t get_le(const uint8_t *b, int nbytes) {
 typedef struct {
   uint32_t n, W, M;
   uint64_t N, B, G;
-  uint32_t f[256];
+  uint32_t kind;        /* 0: "RCL1" static 8-bit model; 1: "RCA1" adaptive model set, 16-bit symbols */
+  uint32_t f[256];      /* kind 0 */
+  uint32_t K;           /* kind 1: model set (see "Adaptive coding" below) */
+  uint32_t *mbase, *mlen, *mf;
   uint32_t final_state[32];
   uint64_t *offset;     /* M-1 */
   uint64_t *maxg;       /* M-1 */
@@ -461,6 +475,9 @@ typedef struct {
 } or_box;
 
 static void box_free(or_box *b) {
+  free(b->mbase);
+  free(b->mlen);
+  free(b->mf);
   free(b->offset);
   free(b->maxg);
   free(b->state);
@@ -472,9 +489,12 @@ static int box_write(const or_box *bx, const uint16_t *words, uint8_t *out, uint
   uint32_t M = bx->M, W = bx->W;
   uint64_t P = M - 1;
   uint32_t count = 0;
+  uint64_t msum = 0;
   for (int s = 0; s < 256; ++s) count += bx->f[s] ? 1 : 0;
-  /* sizes */
-  uint64_t header = 28, model = 2 + 5ull * count, finals = 4ull * W;
+  for (uint32_t k = 0; bx->kind == 1 && k < bx->K; ++k) msum += bx->mlen[k];
+  /* sizes; adaptive model block: u32 K, K x (u32 base, u32 len), sum(len) x u32 f */
+  uint64_t header = 28, finals = 4ull * W;
+  uint64_t model = bx->kind == 1 ? 4 + 8ull * bx->K + 4 * msum : 2 + 5ull * count;
   int64_t *d_off = (int64_t *)calloc(P + 1, sizeof(int64_t));
   int64_t *d_g = (int64_t *)calloc(P + 1, sizeof(int64_t));
   if (!d_off || !d_g) { free(d_off); free(d_g); return OR_E_NOMEM; }
@@ -510,23 +530,33 @@ static int box_write(const or_box *bx, const uint16_t *words, uint8_t *out, uint
   if (*len < total) { *len = total; free(d_off); free(d_g); return OR_E_BUFFER; }
   memset(out, 0, total);
   uint8_t *q = out;
-  memcpy(q, "RCL1", 4);
+  memcpy(q, bx->kind == 1 ? "RCA1" : "RCL1", 4);
   q[4] = 1;  /* version */
-  q[5] = 8;  /* symbol bits */
+  q[5] = bx->kind == 1 ? 16 : 8;  /* symbol bits (8 or 16) */
   q[6] = (uint8_t)bx->n;
   q[7] = (uint8_t)W;
   put_le(q + 8, M, 4);
   put_le(q + 12, bx->N, 8);
   put_le(q + 20, bx->B, 8); /* M, B, N stored as-is */
   q += header;
-  put_le(q, count, 2);
-  q += 2;
-  for (int s = 0; s < 256; ++s)
-    if (bx->f[s]) {
-      q[0] = (uint8_t)s;
-      put_le(q + 1, bx->f[s], 4);
-      q += 5;
+  if (bx->kind == 1) {
+    put_le(q, bx->K, 4);
+    q += 4;
+    for (uint32_t k = 0; k < bx->K; ++k, q += 8) {
+      put_le(q, bx->mbase[k], 4);
+      put_le(q + 4, bx->mlen[k], 4);
     }
+    for (uint64_t e = 0; e < msum; ++e, q += 4) put_le(q, bx->mf[e], 4);
+  } else {
+    put_le(q, count, 2);
+    q += 2;
+    for (int s = 0; s < 256; ++s)
+      if (bx->f[s]) {
+        q[0] = (uint8_t)s;
+        put_le(q + 1, bx->f[s], 4);
+        q += 5;
+      }
+  }
   for (uint32_t j = 0; j < W; ++j, q += 4) put_le(q, bx->final_state[j], 4);
   uint64_t bp = or_pack_series(d_off, P, 1, 5, q, 0);
   bp = or_pack_series(d_g, P, 1, 5, q, bp);
@@ -545,8 +575,10 @@ static int box_write(const or_box *bx, const uint16_t *words, uint8_t *out, uint
 
 static int box_read(const uint8_t *c, uint64_t len, or_box *bx) {
   memset(bx, 0, sizeof(*bx));
-  if (len < 28 || memcmp(c, "RCL1", 4) != 0) return OR_E_CONTAINER;
-  if (c[4] != 1 || c[5] != 8) return OR_E_CONTAINER;
+  if (len < 28) return OR_E_CONTAINER;
+  if (memcmp(c, "RCL1", 4) == 0 && c[4] == 1 && c[5] == 8) bx->kind = 0;
+  else if (memcmp(c, "RCA1", 4) == 0 && c[4] == 1 && c[5] == 16) bx->kind = 1;
+  else return OR_E_CONTAINER;
   bx->n = c[6];
   bx->W = c[7];
   bx->M = (uint32_t)get_le(c + 8, 4);
@@ -555,19 +587,48 @@ static int box_read(const uint8_t *c, uint64_t len, or_box *bx) {
   if (bx->n < 1 || bx->n > 16 || bx->W < 1 || bx->W > 32 || bx->M < 1) return OR_E_CONTAINER;
   bx->G = ceil_div(bx->N, bx->W);
   uint64_t pos = 28;
-  if (pos + 2 > len) return OR_E_CONTAINER;
-  uint32_t count = (uint32_t)get_le(c + pos, 2);
-  pos += 2;
-  if (pos + 5ull * count > len) return OR_E_CONTAINER;
-  uint64_t fsum = 0;
-  for (uint32_t k = 0; k < count; ++k, pos += 5) {
-    bx->f[c[pos]] = (uint32_t)get_le(c + pos + 1, 4);
-    fsum += bx->f[c[pos]];
+  if (bx->kind == 1) {
+    if (pos + 4 > len) return OR_E_CONTAINER;
+    bx->K = (uint32_t)get_le(c + pos, 4);
+    pos += 4;
+    if (bx->K < 1 || bx->K > 256 || pos + 8ull * bx->K > len) return OR_E_CONTAINER;
+    bx->mbase = (uint32_t *)calloc(bx->K, 4);
+    bx->mlen = (uint32_t *)calloc(bx->K, 4);
+    if (!bx->mbase || !bx->mlen) { box_free(bx); return OR_E_NOMEM; }
+    uint64_t msum = 0;
+    for (uint32_t k = 0; k < bx->K; ++k, pos += 8) {
+      bx->mbase[k] = (uint32_t)get_le(c + pos, 4);
+      bx->mlen[k] = (uint32_t)get_le(c + pos + 4, 4);
+      if (bx->mlen[k] < 1 || (uint64_t)bx->mbase[k] + bx->mlen[k] > 65536) { box_free(bx); return OR_E_CONTAINER; }
+      msum += bx->mlen[k];
+    }
+    if (pos + 4 * msum > len) { box_free(bx); return OR_E_CONTAINER; }
+    bx->mf = (uint32_t *)calloc(msum + 1, 4);
+    if (!bx->mf) { box_free(bx); return OR_E_NOMEM; }
+    for (uint64_t e = 0; e < msum; ++e, pos += 4) bx->mf[e] = (uint32_t)get_le(c + pos, 4);
+    uint64_t e0 = 0;
+    for (uint32_t k = 0; k < bx->K; ++k) { /* every model sums to 2^n */
+      uint64_t fsum = 0;
+      for (uint32_t j = 0; j < bx->mlen[k]; ++j) fsum += bx->mf[e0 + j];
+      e0 += bx->mlen[k];
+      if (fsum != (1ull << bx->n)) { box_free(bx); return OR_E_CONTAINER; }
+    }
+    bx->model_bytes = 4 + 8ull * bx->K + 4 * msum;
+  } else {
+    if (pos + 2 > len) return OR_E_CONTAINER;
+    uint32_t count = (uint32_t)get_le(c + pos, 2);
+    pos += 2;
+    if (pos + 5ull * count > len) return OR_E_CONTAINER;
+    uint64_t fsum = 0;
+    for (uint32_t k = 0; k < count; ++k, pos += 5) {
+      bx->f[c[pos]] = (uint32_t)get_le(c + pos + 1, 4);
+      fsum += bx->f[c[pos]];
+    }
+    if (fsum != (1ull << bx->n)) return OR_E_CONTAINER;
+    bx->model_bytes = 2 + 5ull * count;
   }
-  if (fsum != (1ull << bx->n)) return OR_E_CONTAINER;
-  bx->model_bytes = 2 + 5ull * count;
   bx->header_bytes = 28;
-  if (pos + 4ull * bx->W > len) return OR_E_CONTAINER;
+  if (pos + 4ull * bx->W > len) { box_free(bx); return OR_E_CONTAINER; }
   for (uint32_t j = 0; j < bx->W; ++j, pos += 4) bx->final_state[j] = (uint32_t)get_le(c + pos, 4);
   uint64_t meta_start = pos;
   uint64_t P = bx->M - 1, W = bx->W;
@@ -749,6 +810,7 @@ int or_container_points(const uint8_t *c, uint64_t len, uint64_t *offset, uint64
  * [sync_start(point t), sync_start(point t+1) - 1] (Z13). */
 static int box_task(const or_box *bx, const uint16_t *w, uint32_t t, uint8_t *out, uint64_t *lo_out,
                     uint64_t *hi_out) {
+  if (bx->kind != 0) return OR_E_ARG; /* adaptive containers: or_ad_recoil_decode* (needs the model ids) */
   uint32_t W = bx->W;
   uint32_t st[32];
   int64_t ig[32];
@@ -909,5 +971,315 @@ int or_partitioned_decode(const uint8_t *c, uint64_t len, uint8_t *out) {
     base += b;
   }
   free(words);
+  return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* Adaptive coding: index-keyed models, 16-bit symbols                 */
+/* (P:227 item (3); P:411 sizeof(s_i) = 8 or 16 bits)           */
+/* ------------------------------------------------------------------ */
+
+/* A model set has K models.  Model k covers the symbol values base[k] ..
+ * base[k] + len[k] - 1 with frequencies mf[off_k + j] (sum 2^n; 0 = not in
+ * the model), off_k = len[0] + ... + len[k-1].  Symbol i is coded with
+ * model mid[i] -- the "symbol index as a key" of P:227 -- and Eq. 1-4 are
+ * used unchanged with f, F of that model.  The renormalisation before
+ * symbol i (Eq. 3) uses f of model mid[i], so the split metadata (events,
+ * backward scan, H, series) is exactly that of the static codec. */
+typedef struct {
+  uint32_t K;
+  const uint32_t *base, *len, *mf;
+  uint64_t *off;  /* K + 1 */
+  uint32_t *F;    /* per entry: F_k(j) = sum of mf[off_k .. off_k + j - 1] */
+} or_ad_models;
+
+static int ad_models_init(or_ad_models *m, uint32_t K, const uint32_t *base, const uint32_t *len,
+                          const uint32_t *mf, uint32_t n) {
+  memset(m, 0, sizeof(*m));
+  if (K < 1 || K > 256) return OR_E_ARG;
+  m->K = K;
+  m->base = base;
+  m->len = len;
+  m->mf = mf;
+  m->off = (uint64_t *)calloc(K + 1, 8);
+  if (!m->off) return OR_E_NOMEM;
+  for (uint32_t k = 0; k < K; ++k) {
+    if (len[k] < 1 || (uint64_t)base[k] + len[k] > 65536) { free(m->off); return OR_E_MODEL; }
+    m->off[k + 1] = m->off[k] + len[k];
+  }
+  m->F = (uint32_t *)calloc(m->off[K] + 1, 4);
+  if (!m->F) { free(m->off); return OR_E_NOMEM; }
+  for (uint32_t k = 0; k < K; ++k) {
+    uint64_t acc = 0;
+    for (uint32_t j = 0; j < len[k]; ++j) {
+      m->F[m->off[k] + j] = (uint32_t)acc;
+      acc += mf[m->off[k] + j];
+    }
+    if (acc != (1ull << n)) { free(m->off); free(m->F); return OR_E_MODEL; }
+  }
+  return OR_OK;
+}
+
+static void ad_models_free(or_ad_models *m) {
+  free(m->off);
+  free(m->F);
+}
+
+/* f and F of symbol value v under model k; 0 if v is not in the model */
+static int ad_fF(const or_ad_models *m, uint32_t k, uint32_t v, uint32_t *f, uint32_t *F) {
+  if (k >= m->K || v < m->base[k] || v - m->base[k] >= m->len[k]) return 0;
+  uint64_t e = m->off[k] + (v - m->base[k]);
+  *f = m->mf[e];
+  *F = m->F[e];
+  return *f > 0;
+}
+
+/* Eq. 2 under model k: the value v with F_k(v) <= x mod 2^n < F_k(v) + f_k(v),
+ * by a plain scan of the model's entries. */
+static int ad_decode_step(const or_ad_models *m, uint32_t k, uint32_t n, uint64_t *x, uint32_t *v) {
+  uint32_t slot = (uint32_t)(*x & ((1u << n) - 1));
+  for (uint32_t j = 0; j < m->len[k]; ++j) {
+    uint64_t e = m->off[k] + j;
+    if (m->mf[e] && m->F[e] <= slot && slot < m->F[e] + m->mf[e]) {
+      *x = (uint64_t)m->mf[e] * (*x >> n) - m->F[e] + slot;
+      *v = m->base[k] + j;
+      return OR_OK;
+    }
+  }
+  return OR_E_MODEL;
+}
+
+/* The interleaved encoder of P:166-170 (see or_interleaved_encode) with the
+ * model of every symbol taken from mid[i]. */
+int64_t or_ad_interleaved_encode(const uint16_t *sym, uint64_t N, const uint8_t *mid, uint32_t K,
+                                 const uint32_t *base, const uint32_t *len, const uint32_t *mf, uint32_t n,
+                                 uint32_t W, uint16_t *words, uint32_t *final_states, or_event *events) {
+  if (W < 1 || W > 32 || n < 1 || n > 16) return OR_E_ARG;
+  or_ad_models m;
+  int rc = ad_models_init(&m, K, base, len, mf, n);
+  if (rc) return rc;
+  uint32_t f, F;
+  for (uint64_t i = 0; i < N; ++i)
+    if (!ad_fF(&m, mid[i], sym[i], &f, &F)) { ad_models_free(&m); return OR_E_MODEL; }
+  uint64_t x[32];
+  for (uint32_t j = 0; j < W; ++j) x[j] = L_BOUND;
+  uint64_t G = (N + W - 1) / W, p = 0;
+  for (uint64_t g = 0; g < G; ++g) {
+    for (uint32_t j = 0; j < W; ++j) { /* renormalisation outputs, increasing lane ID (Z4) */
+      uint64_t i = g * W + j;
+      if (i >= N) continue;
+      ad_fF(&m, mid[i], sym[i], &f, &F);
+      uint64_t p_before = p;
+      or_renorm_encode(&x[j], f, n, words, &p);
+      for (uint64_t q = p_before; q < p; ++q)
+        if (events) {
+          events[q].idx = (int64_t)i - (int64_t)W;
+          events[q].lane = j;
+          events[q].state = (uint32_t)x[j];
+        }
+    }
+    for (uint32_t j = 0; j < W; ++j) { /* Eq. 1 */
+      uint64_t i = g * W + j;
+      if (i >= N) continue;
+      ad_fF(&m, mid[i], sym[i], &f, &F);
+      x[j] = or_encode_step(x[j], f, F, n);
+      if (x[j] >> 32) { ad_models_free(&m); return OR_E_OVERFLOW; }
+    }
+  }
+  for (uint32_t j = 0; j < W; ++j) final_states[j] = (uint32_t)x[j];
+  ad_models_free(&m);
+  return (int64_t)p;
+}
+
+/* Serial decoder of the adaptive stream (see or_interleaved_decode). */
+int or_ad_interleaved_decode(const uint16_t *words, uint64_t B, const uint32_t *final_states, uint64_t N,
+                             const uint8_t *mid, uint32_t K, const uint32_t *base, const uint32_t *len,
+                             const uint32_t *mf, uint32_t n, uint32_t W, uint16_t *out) {
+  if (W < 1 || W > 32) return OR_E_ARG;
+  or_ad_models m;
+  int rc = ad_models_init(&m, K, base, len, mf, n);
+  if (rc) return rc;
+  uint64_t x[32];
+  for (uint32_t j = 0; j < W; ++j) x[j] = final_states[j];
+  int64_t p = (int64_t)B - 1;
+  int64_t G = (int64_t)((N + W - 1) / W);
+  for (int64_t g = G - 1; g >= -1 && rc == OR_OK; --g) {
+    for (int32_t j = (int32_t)W - 1; j >= 0; --j)
+      if (or_renorm_decode(&x[j], words, &p) < 0) { rc = OR_E_UNDERFLOW; break; }
+    if (g < 0 || rc) break;
+    for (uint32_t j = 0; j < W && rc == OR_OK; ++j) {
+      uint64_t i = (uint64_t)g * W + j;
+      if (i >= N) continue;
+      uint32_t v;
+      if (mid[i] >= K) { rc = OR_E_MODEL; break; }
+      rc = ad_decode_step(&m, mid[i], n, &x[j], &v);
+      out[i] = (uint16_t)v;
+    }
+  }
+  ad_models_free(&m);
+  if (rc) return rc;
+  if (p != -1) return OR_E_END;
+  for (uint32_t j = 0; j < W; ++j)
+    if (x[j] != L_BOUND) return OR_E_END;
+  return OR_OK;
+}
+
+/* The 3-phase task decoder of P:303-315 (see or_decode_from) for the
+ * adaptive codec. */
+int or_ad_decode_from(const uint16_t *words, const uint8_t *mid, uint32_t K, const uint32_t *base,
+                      const uint32_t *len, const uint32_t *mf, uint32_t n, uint32_t W, uint64_t N,
+                      int64_t cursor0, int64_t start_group, const uint32_t *init_state,
+                      const int64_t *init_group, uint64_t commit_lo, uint64_t commit_hi, uint16_t *out) {
+  or_ad_models m;
+  int rc = ad_models_init(&m, K, base, len, mf, n);
+  if (rc) return rc;
+  uint64_t x[32] = {0};
+  int inited[32] = {0};
+  int64_t p = cursor0;
+  int64_t lo_group = (int64_t)(commit_lo / W);
+  for (int64_t g = start_group; g >= lo_group && rc == OR_OK; --g) {
+    for (int32_t j = (int32_t)W - 1; j >= 0; --j) {
+      if (!inited[j] && init_group[j] == g) {
+        x[j] = init_state[j];
+        inited[j] = 1;
+      }
+      if (inited[j] && or_renorm_decode(&x[j], words, &p) < 0) { rc = OR_E_UNDERFLOW; break; }
+    }
+    for (uint32_t j = 0; j < W && rc == OR_OK; ++j) {
+      uint64_t i = (uint64_t)g * W + j;
+      if (!inited[j] || i >= N) continue;
+      uint32_t v;
+      if (mid[i] >= K) { rc = OR_E_MODEL; break; }
+      rc = ad_decode_step(&m, mid[i], n, &x[j], &v);
+      if (rc == OR_OK && i >= commit_lo && i <= commit_hi) out[i] = (uint16_t)v;
+    }
+  }
+  if (rc == OR_OK && commit_lo == 0) {
+    for (int32_t j = (int32_t)W - 1; j >= 0 && rc == OR_OK; --j)
+      if (inited[j] && or_renorm_decode(&x[j], words, &p) < 0) rc = OR_E_UNDERFLOW;
+    if (rc == OR_OK) {
+      if (p != -1) rc = OR_E_END;
+      for (uint32_t j = 0; j < W; ++j)
+        if (!inited[j] || x[j] != L_BOUND) rc = OR_E_END;
+    }
+  }
+  ad_models_free(&m);
+  return rc;
+}
+
+/* Recoil container of an adaptive stream ("RCA1": 16-bit symbols, the model
+ * set in the model block; everything else as "RCL1"). */
+int or_ad_recoil_encode(const uint16_t *sym, uint64_t N, const uint8_t *mid, uint32_t K, const uint32_t *base,
+                        const uint32_t *len, const uint32_t *mf, uint32_t n, uint32_t W, uint32_t M,
+                        uint8_t *out, uint64_t *outlen) {
+  if (M < 1 || W < 1 || W > 32 || n < 1 || n > 16 || K < 1 || K > 256) return OR_E_ARG;
+  uint16_t *words = (uint16_t *)malloc(2 * N + 2);
+  or_event *ev = (or_event *)malloc(sizeof(or_event) * (N + 1));
+  uint64_t *chosen = (uint64_t *)malloc(8ull * M);
+  if (!words || !ev || !chosen) { free(words); free(ev); free(chosen); return OR_E_NOMEM; }
+  or_box bx;
+  memset(&bx, 0, sizeof(bx));
+  bx.kind = 1;
+  bx.n = n;
+  bx.W = W;
+  bx.N = N;
+  bx.G = ceil_div(N, W);
+  bx.K = K;
+  uint64_t msum = 0;
+  for (uint32_t k = 0; k < K; ++k) msum += len[k];
+  bx.mbase = (uint32_t *)malloc(4ull * K);
+  bx.mlen = (uint32_t *)malloc(4ull * K);
+  bx.mf = (uint32_t *)malloc(4 * msum + 4);
+  int64_t B = (!bx.mbase || !bx.mlen || !bx.mf) ? OR_E_NOMEM
+              : or_ad_interleaved_encode(sym, N, mid, K, base, len, mf, n, W, words, bx.final_state, ev);
+  if (B < 0) { box_free(&bx); free(words); free(ev); free(chosen); return (int)B; }
+  memcpy(bx.mbase, base, 4ull * K);
+  memcpy(bx.mlen, len, 4ull * K);
+  memcpy(bx.mf, mf, 4 * msum);
+  bx.B = (uint64_t)B;
+  int64_t P = or_choose_splits(ev, bx.B, N, W, M, chosen);
+  bx.M = (uint32_t)P + 1;
+  bx.offset = (uint64_t *)calloc((uint64_t)P + 1, 8);
+  bx.maxg = (uint64_t *)calloc((uint64_t)P + 1, 8);
+  bx.state = (uint32_t *)calloc((uint64_t)P * W + 1, 4);
+  bx.gdiff = (int64_t *)calloc((uint64_t)P * W + 1, 8);
+  for (int64_t k = 0; k < P; ++k) { /* same split records as or_recoil_encode */
+    int64_t ai[32], ss;
+    uint32_t st[32];
+    or_backward_scan(ev, chosen[k], W, st, ai, &ss);
+    bx.offset[k] = chosen[k];
+    bx.maxg[k] = (uint64_t)ev[chosen[k]].idx / W;
+    for (uint32_t j = 0; j < W; ++j) {
+      bx.state[k * W + j] = st[j];
+      bx.gdiff[k * W + j] = (int64_t)bx.maxg[k] - ai[j] / (int64_t)W;
+    }
+  }
+  int rc = box_write(&bx, words, out, outlen);
+  box_free(&bx);
+  free(chosen);
+  free(words);
+  free(ev);
+  return rc;
+}
+
+static int box_task_ad(const or_box *bx, const uint16_t *w, const uint8_t *mid, uint32_t t, uint16_t *out,
+                       uint64_t *lo_out, uint64_t *hi_out) {
+  if (bx->kind != 1) return OR_E_ARG;
+  uint32_t W = bx->W;
+  uint32_t st[32];
+  int64_t ig[32];
+  int64_t cursor0, start_group, ss, bi;
+  uint64_t lo = 0, hi;
+  if (t > 0) {
+    point_span(bx, t - 1, &ss, &bi);
+    lo = (uint64_t)ss;
+  }
+  if (t + 1 < bx->M) {
+    point_span(bx, t, &ss, &bi);
+    hi = (uint64_t)ss - 1;
+    cursor0 = (int64_t)bx->offset[t];
+    start_group = (int64_t)bx->maxg[t];
+    for (uint32_t j = 0; j < W; ++j) {
+      st[j] = bx->state[t * W + j];
+      ig[j] = (int64_t)bx->maxg[t] - bx->gdiff[t * W + j];
+    }
+  } else {
+    hi = bx->N - 1;
+    cursor0 = (int64_t)bx->B - 1;
+    start_group = (int64_t)bx->G - 1;
+    for (uint32_t j = 0; j < W; ++j) {
+      st[j] = bx->final_state[j];
+      ig[j] = start_group;
+    }
+  }
+  if (lo_out) *lo_out = lo;
+  if (hi_out) *hi_out = hi;
+  return or_ad_decode_from(w, mid, bx->K, bx->mbase, bx->mlen, bx->mf, bx->n, W, bx->N, cursor0, start_group,
+                           st, ig, lo, hi, out);
+}
+
+int or_ad_recoil_decode(const uint8_t *c, uint64_t len, const uint8_t *mid, uint16_t *out) {
+  or_box bx;
+  int rc = box_read(c, len, &bx);
+  if (rc) return rc;
+  if (bx.kind != 1) { box_free(&bx); return OR_E_ARG; }
+  if (bx.N == 0) { box_free(&bx); return OR_OK; }
+  uint16_t *w = box_words(&bx);
+  for (uint32_t t = 0; t < bx.M && rc == OR_OK; ++t) rc = box_task_ad(&bx, w, mid, t, out, NULL, NULL);
+  free(w);
+  box_free(&bx);
+  return rc;
+}
+
+int or_ad_recoil_decode_task(const uint8_t *c, uint64_t len, const uint8_t *mid, uint32_t task, uint16_t *out,
+                             uint64_t *lo, uint64_t *hi) {
+  or_box bx;
+  int rc = box_read(c, len, &bx);
+  if (rc) return rc;
+  if (bx.kind != 1 || task >= bx.M || bx.N == 0) { box_free(&bx); return OR_E_ARG; }
+  uint16_t *w = box_words(&bx);
+  rc = box_task_ad(&bx, w, mid, task, out, lo, hi);
+  free(w);
+  box_free(&bx);
   return rc;
 }

@@ -39,6 +39,7 @@ typedef struct {
 } or_event;
 
 /* model */
+int or_quantize(const uint64_t *hist, uint32_t count, uint32_t n, uint32_t *f);
 int or_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]);
 uint64_t or_encode_step(uint64_t x, uint32_t f, uint32_t F, uint32_t n);
 int or_decode_step(uint32_t x, const uint32_t f[256], uint32_t n, uint32_t *s, uint32_t *x_prev);
@@ -95,5 +96,26 @@ int or_recoil_decode_tasks(const uint8_t *c, uint64_t len, const uint32_t *tasks
 int or_partitioned_encode(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
                           uint32_t W, uint32_t P, uint8_t *out, uint64_t *len);
 int or_partitioned_decode(const uint8_t *c, uint64_t len, uint8_t *out);
+
+/* Adaptive coding with index-keyed models and 16-bit symbols (P:227 item
+ * (3)): K models, model k = values base[k] .. base[k]+len[k]-1
+ * with frequencies mf[off_k + j] (sum 2^n); symbol i uses model mid[i].
+ * Container "RCA1" (16-bit symbols, model set in the model block). */
+int64_t or_ad_interleaved_encode(const uint16_t *sym, uint64_t N, const uint8_t *mid, uint32_t K,
+                                 const uint32_t *base, const uint32_t *len, const uint32_t *mf, uint32_t n,
+                                 uint32_t W, uint16_t *words, uint32_t *final_states, or_event *events);
+int or_ad_interleaved_decode(const uint16_t *words, uint64_t B, const uint32_t *final_states, uint64_t N,
+                             const uint8_t *mid, uint32_t K, const uint32_t *base, const uint32_t *len,
+                             const uint32_t *mf, uint32_t n, uint32_t W, uint16_t *out);
+int or_ad_decode_from(const uint16_t *words, const uint8_t *mid, uint32_t K, const uint32_t *base,
+                      const uint32_t *len, const uint32_t *mf, uint32_t n, uint32_t W, uint64_t N,
+                      int64_t cursor0, int64_t start_group, const uint32_t *init_state,
+                      const int64_t *init_group, uint64_t commit_lo, uint64_t commit_hi, uint16_t *out);
+int or_ad_recoil_encode(const uint16_t *sym, uint64_t N, const uint8_t *mid, uint32_t K, const uint32_t *base,
+                        const uint32_t *len, const uint32_t *mf, uint32_t n, uint32_t W, uint32_t M,
+                        uint8_t *out, uint64_t *outlen);
+int or_ad_recoil_decode(const uint8_t *c, uint64_t len, const uint8_t *mid, uint16_t *out);
+int or_ad_recoil_decode_task(const uint8_t *c, uint64_t len, const uint8_t *mid, uint32_t task, uint16_t *out,
+                             uint64_t *lo, uint64_t *hi);
 
 #endif

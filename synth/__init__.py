@@ -49,6 +49,10 @@ def _load():
         lib.synth_fill.restype = ctypes.c_int
         lib.synth_u64.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         lib.synth_u64.restype = None
+        lib.synth_fill_models.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_int]
+        lib.synth_fill_models.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -169,3 +173,100 @@ def workload(kind: str, n: int, seed: int, lam: float = 50.0) -> np.ndarray:
 
 def histogram(sym: np.ndarray) -> np.ndarray:
     return np.bincount(sym, minlength=256).astype(np.uint64)
+
+
+# --- latent workload: 16-bit symbols with index-keyed Gaussian models -------------------
+# (div2k through mbt2018-mean, 16-bit symbols, each modelled by a Gaussian
+# whose scale comes from the hyperprior; NEXT rows 1 + 4 of SURVEY.md §8(f)).
+# The hyperprior itself is out of scope: scales are synthetic.  Recipe (DESIGN.md
+# "Input recipe"): K = 64 scale classes sigma_k = exp(linspace(ln 0.11, ln 32, 64))
+# (a compressai-style scale table, capped at 32); model k covers the residuals
+# d in [-R_k, R_k], R_k = ceil(4.5 sigma_k) + 1, as 16-bit values 32768 + d; its
+# integer histogram is the discretised Gaussian mass of each d (the two ends
+# absorb the tails) scaled to 2^40, floored at 1.  Model ids: the flattened
+# latent is C = 192 channels x 64 x 64; channel c has a base class a_c =
+# floor(64 u_c^2) (most channels small-scale), every 8 x 8 spatial tile t an
+# offset b_t in {-4..4}; class = clamp(a_c + b_t, 0, 63).
+
+LATENT_K = 64
+LATENT_CENTER = 32768
+LATENT_C, LATENT_H, LATENT_W = 192, 64, 64
+
+
+def latent_scales(K: int = LATENT_K) -> list[float]:
+    return [math.exp(math.log(0.11) + (math.log(32.0) - math.log(0.11)) * k / (K - 1)) for k in range(K)]
+
+
+def gaussian_hist(sigma: float) -> tuple[int, list[int]]:
+    """-> (R, integer histogram over d = -R..R)."""
+    R = int(math.ceil(4.5 * sigma)) + 1
+    def Phi(x):
+        return 0.5 * math.erfc(-x / math.sqrt(2.0))
+    hist = []
+    for d in range(-R, R + 1):
+        lo = 0.0 if d == -R else Phi((d - 0.5) / sigma)
+        hi = 1.0 if d == R else Phi((d + 0.5) / sigma)
+        hist.append(max(1, int(round((hi - lo) * (1 << 40)))))
+    return R, hist
+
+
+def latent_model_hists(K: int = LATENT_K):
+    """-> {"base": u32[K], "len": u32[K], "hist": [u64 array per model]}"""
+    base, ln, hists = [], [], []
+    for sg in latent_scales(K):
+        R, h = gaussian_hist(sg)
+        base.append(LATENT_CENTER - R)
+        ln.append(2 * R + 1)
+        hists.append(np.array(h, dtype=np.uint64))
+    return {"base": np.array(base, dtype=np.uint32), "len": np.array(ln, dtype=np.uint32), "hist": hists}
+
+
+def latent_model_ids(n: int, seed: int, K: int = LATENT_K) -> np.ndarray:
+    """Per-index model ids (the decoder-side 'hyperprior' output), see the recipe above."""
+    i = np.arange(int(n), dtype=np.int64)
+    plane = LATENT_H * LATENT_W
+    ch = i // plane                       # global channel counter (images repeat every C channels)
+    y = (i % plane) // LATENT_W
+    x = i % LATENT_W
+    tile = ch * (plane // 64) + (y // 8) * (LATENT_W // 8) + (x // 8)
+    n_ch = int(ch[-1]) + 1 if n else 0
+    n_tile = int(tile[-1]) + 1 if n else 0
+    uc = u64(n_ch, seed ^ 0xA5A5A5A5) if n else np.zeros(0, np.uint64)
+    ut = u64(n_tile, seed ^ 0x5A5A5A5A) if n else np.zeros(0, np.uint64)
+    a = np.floor(K * ((uc >> np.uint64(11)).astype(np.float64) / float(1 << 53)) ** 2).astype(np.int64)
+    b = (ut % np.uint64(9)).astype(np.int64) - 4
+    return np.clip(a[ch] + b[tile], 0, K - 1).astype(np.uint8)
+
+
+def latent_symbols(mid: np.ndarray, seed: int, hists=None, threads: int | None = None) -> np.ndarray:
+    """16-bit symbols drawn from the models' integer histograms (exact inverse CDF)."""
+    if hists is None:
+        hists = latent_model_hists()
+    thr, off = [], [0]
+    for h in hists["hist"]:
+        tot = int(h.sum())
+        acc = 0
+        for v in h.tolist():
+            acc += int(v)
+            thr.append(min(TWO64 - 1, (acc * TWO64) // tot))
+        thr[-1] = TWO64 - 1
+        off.append(off[-1] + len(h))
+    thr = np.array(thr, dtype=np.uint64)
+    off = np.array(off, dtype=np.uint64)
+    base = np.ascontiguousarray(hists["base"], dtype=np.uint32)
+    ln = np.ascontiguousarray(hists["len"], dtype=np.uint32)
+    mid = np.ascontiguousarray(mid, dtype=np.uint8)
+    out = np.empty(mid.size, dtype=np.uint16)
+    if mid.size:
+        if threads is None:
+            threads = max(1, min(16, os.cpu_count() or 1))
+        _load().synth_fill_models(out.ctypes.data, mid.ctypes.data, 0, mid.size, seed & (TWO64 - 1), thr.ctypes.data,
+                                  off.ctypes.data, base.ctypes.data, ln.ctypes.data, threads)
+    return out
+
+
+def latent_workload(n: int, seed: int):
+    """-> (symbols u16[n], model ids u8[n], model histograms)"""
+    hists = latent_model_hists()
+    mid = latent_model_ids(n, seed)
+    return latent_symbols(mid, seed, hists), mid, hists

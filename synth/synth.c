@@ -93,3 +93,51 @@ int synth_fill(uint8_t *out, uint64_t start, uint64_t count, uint64_t seed,
 void synth_u64(uint64_t *out, uint64_t start, uint64_t count, uint64_t seed) {
   for (uint64_t i = 0; i < count; ++i) out[i] = mix64(seed + (start + i + 1) * GAMMA);
 }
+
+/* Index-keyed draws for the adaptive workload: value_i = base[k] + j where
+ * k = mid[i] and j = #{t < len[k] : thr[off[k] + t] <= u_i} (clamped), u_i the
+ * SplitMix64 draw i.  thr: per model, len[k] non-decreasing cumulative
+ * thresholds scaled to 2^64.  threads <= 0 means 1. */
+typedef struct {
+  uint16_t *out;
+  const uint8_t *mid;
+  uint64_t begin, end, seed;
+  const uint64_t *thr, *off;
+  const uint32_t *base, *len;
+} ljob_t;
+
+static void *run_ljob(void *arg) {
+  ljob_t *j = (ljob_t *)arg;
+  for (uint64_t i = j->begin; i < j->end; ++i) {
+    uint32_t k = j->mid[i - j->begin];
+    const uint64_t *t = j->thr + j->off[k];
+    uint64_t u = mix64(j->seed + (i + 1) * GAMMA);
+    uint32_t lo = 0, hi = j->len[k] - 1; /* first t with u < thr[t] */
+    while (lo < hi) {
+      uint32_t m = (lo + hi) >> 1;
+      if (t[m] <= u) lo = m + 1; else hi = m;
+    }
+    j->out[i - j->begin] = (uint16_t)(j->base[k] + lo);
+  }
+  return NULL;
+}
+
+int synth_fill_models(uint16_t *out, const uint8_t *mid, uint64_t start, uint64_t count, uint64_t seed,
+                      const uint64_t *thr, const uint64_t *off, const uint32_t *base, const uint32_t *len,
+                      int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  if (count < (1u << 20)) threads = 1;
+  pthread_t th[64];
+  ljob_t jobs[64];
+  for (int t = 0; t < threads; ++t) {
+    uint64_t b = count * (uint64_t)t / (uint64_t)threads;
+    uint64_t e = count * (uint64_t)(t + 1) / (uint64_t)threads;
+    ljob_t jb = {out + b, mid + b, start + b, start + e, seed, thr, off, base, len};
+    jobs[t] = jb;
+  }
+  for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, run_ljob, &jobs[t]);
+  run_ljob(&jobs[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}

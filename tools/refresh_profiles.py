@@ -1,0 +1,68 @@
+"""Turn ncu --set full captures (gpurun_out/prof_<config>_<tag>.ncu-rep) into the
+committed summaries under profiles/ and the per-launch numbers bench.py reads
+(profiles/ncu_traffic.json): DRAM bytes and shared-memory wavefronts per launch.
+
+usage: python tools/refresh_profiles.py TAG config2:7104 config1:16 config3:14208 ...
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__maximum_warps_per_active_cycle_pct",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "smsp__cycles_active.avg", "sm__cycles_elapsed.avg.per_second", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "sm__inst_executed.sum", "launch__shared_mem_per_block_static"]
+
+
+def summary(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    out = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
+    for w in WANT:
+        if w in hdr:
+            i = hdr.index(w)
+            v = vals[i].replace(",", "")
+            try:
+                v = float(v)
+            except ValueError:
+                pass
+            out[w] = {"value": v, "unit": units[i]}
+    return out
+
+
+def main():
+    tag = sys.argv[1]
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(tf)) if os.path.exists(tf) else {}
+    for spec in sys.argv[2:]:
+        cfg, M = spec.split(":")
+        rep = os.path.join(ROOT, "gpurun_out", f"prof_{cfg}_{tag}.ncu-rep")
+        s = summary(rep)
+        s["source"] = f"ncu --set full --clock-control none, 1 decode launch of bench.py --config {cfg} ({M} splits)"
+        dst = os.path.join(ROOT, "profiles", f"r01_decode_{cfg}_ncu_full.json")
+        json.dump(s, open(dst, "w"), indent=1)
+        rd = s["dram__bytes_read.sum"]["value"] * UNIT[s["dram__bytes_read.sum"]["unit"]]
+        wr = s["dram__bytes_write.sum"]["value"] * UNIT[s["dram__bytes_write.sum"]["unit"]]
+        wf = s["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]["value"]
+        traffic[f"{cfg}:{M}"] = {"dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
+                                 "smem_wavefronts_per_launch": int(wf),
+                                 "source": os.path.relpath(dst, ROOT) + " (ncu --set full, 1 launch inside bench.py)"}
+        print(cfg, M, int(rd + wr), int(wf), s["gpu__time_duration.sum"])
+    json.dump(traffic, open(tf, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
