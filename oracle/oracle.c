@@ -299,18 +299,23 @@ int64_t or_choose_splits(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t
     int64_t T = (int64_t)ceil_div(N - (uint64_t)(prev + 1), M - m + 1);
     while (first < n_ev && ev[first].idx <= prev) first++;
     int64_t best = -1, best_h = 0;
-    for (uint64_t e = first; e < n_ev && ev[e].idx - prev <= 2 * T; ++e) {
-      int64_t ss;
-      if (!or_backward_scan(ev, e, W, st, ai, &ss)) continue;
-      if (ss <= prev) continue;
-      if (ev[e].idx / W - ss / W > 65535) continue;
-      int64_t t = ev[e].idx - prev;
-      int64_t ts = ev[e].idx - ss + 1;
-      int64_t h = or_heuristic(t, ts, T);
-      if (best < 0 || h < best_h) {
-        best = (int64_t)e;
-        best_h = h;
+    /* candidates with 0 < t <= 2T; a window without a feasible candidate is
+     * doubled until one is found or the stream ends (reading Z10'') */
+    for (int64_t limit = 2 * T; best < 0; limit *= 2) {
+      for (uint64_t e = first; e < n_ev && ev[e].idx - prev <= limit; ++e) {
+        int64_t ss;
+        if (!or_backward_scan(ev, e, W, st, ai, &ss)) continue;
+        if (ss <= prev) continue;
+        if (ev[e].idx / W - ss / W > 65535) continue;
+        int64_t t = ev[e].idx - prev;
+        int64_t ts = ev[e].idx - ss + 1;
+        int64_t h = or_heuristic(t, ts, T);
+        if (best < 0 || h < best_h) {
+          best = (int64_t)e;
+          best_h = h;
+        }
       }
+      if (n_ev == 0 || ev[n_ev - 1].idx - prev <= limit) break; /* the window covers the rest */
     }
     if (best < 0) break;
     chosen[count++] = (uint64_t)best;

@@ -63,6 +63,7 @@ class Selector {
   Selector(uint64_t N, uint32_t M) : N_(N), M_(M) {
     done_ = (M <= 1 || N == 0);
     T_ = done_ ? 0 : (int64_t)ceil_div(N, M);
+    win_ = 2 * T_;
     for (uint32_t j = 0; j < kLanes; ++j) {
       last_idx_[j] = -1;
       prev_lane_[j] = next_lane_[j] = -1;
@@ -81,14 +82,14 @@ class Selector {
     last_idx_[lane] = idx;
     if (done_) return;
     int64_t ss = (nseen_ == (int)kLanes) ? last_idx_[tail_] : -1;  // min over the lanes' last events
-    while (!done_ && idx > prev_ + 2 * T_) finalize();
+    while (!done_ && idx > prev_ + win_) finalize(false);
     if (done_) return;
     if (buf_.empty()) buf_base_ = offset;
     buf_.push_back(Ev{idx, ss, (uint16_t)state, (uint8_t)lane});
   }
 
   void finish() {
-    while (!done_) finalize();
+    while (!done_) finalize(true);
   }
 
   struct Point {
@@ -118,13 +119,15 @@ class Selector {
     if (tail_ < 0) tail_ = j;
   }
 
-  // Close the window of boundary m: pick the minimum-H candidate.
-  void finalize() {
+  // Close the window of boundary m: pick the minimum-H candidate with
+  // 0 < t <= win_ (2T, doubled while empty: reading Z10'').  at_end: no more
+  // events will arrive, so an empty window is doubled until it covers the buffer.
+  void finalize(bool at_end) {
     int64_t best = -1, best_h = 0;
     for (size_t q = 0; q < buf_.size(); ++q) {
       const Ev &e = buf_[q];
       if (e.idx <= prev_) continue;
-      if (e.idx - prev_ > 2 * T_) break;
+      if (e.idx - prev_ > win_) break;
       if (e.ss < 0 || e.ss <= prev_) continue;
       if (e.idx / kLanes - e.ss / kLanes > 65535) continue;
       int64_t t = e.idx - prev_, ts = e.idx - e.ss + 1;
@@ -135,8 +138,13 @@ class Selector {
       }
     }
     if (best < 0) {
-      done_ = true;
-      buf_.clear();
+      const bool covers = buf_.empty() || buf_.back().idx - prev_ <= win_;
+      if (at_end && covers) {
+        done_ = true;
+        buf_.clear();
+      } else {
+        win_ *= 2;
+      }
       return;
     }
     // anchors: backward scan from the chosen event over the buffer
@@ -165,13 +173,14 @@ class Selector {
       return;
     }
     T_ = (int64_t)ceil_div(N_ - (uint64_t)(prev_ + 1), M_ - m_ + 1);
+    win_ = 2 * T_;
   }
 
   uint64_t N_;
   uint32_t M_;
   uint32_t m_ = 1;
   bool done_;
-  int64_t T_;
+  int64_t T_, win_;
   int64_t prev_ = -1;
   std::deque<Ev> buf_;
   uint64_t buf_base_ = 0;

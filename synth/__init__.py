@@ -185,8 +185,9 @@ def histogram(sym: np.ndarray) -> np.ndarray:
 # integer histogram is the discretised Gaussian mass of each d (the two ends
 # absorb the tails) scaled to 2^40, floored at 1.  Model ids: the flattened
 # latent is C = 192 channels x 64 x 64; channel c has a base class a_c =
-# floor(64 u_c^2) (most channels small-scale), every 8 x 8 spatial tile t an
-# offset b_t in {-4..4}; class = clamp(a_c + b_t, 0, 63).
+# floor(64 sqrt(u_c)), every 8 x 8 spatial tile t an
+# offset b_t in {-4..4}; class = clamp(a_c + b_t, 0, 63).  Mean entropy ~4.4
+# bit/symbol (div2k801 at n = 16: 2,093 KB of 7,209 KB = 4.64 bit/symbol, tab:datasets).
 
 LATENT_K = 64
 LATENT_CENTER = 32768
@@ -233,7 +234,7 @@ def latent_model_ids(n: int, seed: int, K: int = LATENT_K) -> np.ndarray:
     n_tile = int(tile[-1]) + 1 if n else 0
     uc = u64(n_ch, seed ^ 0xA5A5A5A5) if n else np.zeros(0, np.uint64)
     ut = u64(n_tile, seed ^ 0x5A5A5A5A) if n else np.zeros(0, np.uint64)
-    a = np.floor(K * ((uc >> np.uint64(11)).astype(np.float64) / float(1 << 53)) ** 2).astype(np.int64)
+    a = np.floor(K * np.sqrt((uc >> np.uint64(11)).astype(np.float64) / float(1 << 53))).astype(np.int64)
     b = (ut % np.uint64(9)).astype(np.int64) - 4
     return np.clip(a[ch] + b[tile], 0, K - 1).astype(np.uint8)
 
