@@ -66,6 +66,12 @@ const char *recoil_strerror(int status);
  * raise) taken from the largest f (ties: smaller count, then smaller symbol).
  * hist: 256 counts.  freqs_out: 256 entries.  Errors: E_ARG (n outside 1..16),
  * E_EMPTY, E_ALPHABET. */
+/* Reading Z19's quantiser over `count` entries (recoil_build_model = 256):
+ * f = floor(hist 2^n / total), present entries raised to 1, shortfall by
+ * largest remainder (ties: lower index), excess from the largest f.  Used for
+ * the per-model frequencies of the adaptive codec.  Errors as recoil_build_model. */
+int recoil_quantize(const uint64_t *hist, uint32_t count, uint32_t prob_bits, uint32_t *freqs_out);
+
 int recoil_build_model(const uint64_t hist[256], uint32_t prob_bits, uint32_t freqs_out[256]);
 
 /* ---------------------------------------------------------------------- */
@@ -84,6 +90,19 @@ int recoil_build_model(const uint64_t hist[256], uint32_t prob_bits, uint32_t fr
 int recoil_encode(const uint8_t *symbols, uint64_t n_symbols, const uint32_t freqs[256],
                   uint32_t prob_bits, uint32_t n_splits, uint8_t *container,
                   uint64_t *container_len);
+
+/* Adaptive Recoil encode (P:227 item (3)): 16-bit symbols,
+ * symbol i coded with model model_ids[i] < n_models (<= 256).  Model k covers
+ * the values model_base[k] .. model_base[k] + model_len[k] - 1 (<= 65535) with
+ * frequencies freqs[off_k + j], off_k = model_len[0] + ... + model_len[k-1],
+ * each model summing to 2^prob_bits.  Same split heuristic and metadata as
+ * recoil_encode; container "RCA1" (the model set replaces the model block).
+ * Errors: E_ARG, E_ZERO_FREQ (a symbol outside its model or with f = 0),
+ * E_OVERFLOW, E_BUFFER, E_NOMEM. */
+int recoil_encode_adaptive(const uint16_t *symbols, uint64_t n_symbols, const uint8_t *model_ids,
+                           uint32_t n_models, const uint32_t *model_base, const uint32_t *model_len,
+                           const uint32_t *freqs, uint32_t prob_bits, uint32_t n_splits, uint8_t *container,
+                           uint64_t *container_len);
 
 /* Decoder-adaptive combine: keep the split points at
  * 1-based positions k, 2k, ... with k = ceil(M / target_splits) and rewrite
@@ -104,6 +123,8 @@ typedef struct {
   uint64_t meta_bytes;   /* final states + split metadata (or offset table + states) */
   uint64_t word_bytes;   /* 2 B */
   uint64_t total_bytes;
+  uint32_t symbol_bits;  /* 8 ("RCL1", "RCV1") or 16 ("RCA1", adaptive) */
+  uint32_t n_models;     /* 1, or K for an adaptive container */
 } recoil_info;
 
 /* Parse and validate a container (either kind).  Errors: container errors. */
@@ -132,9 +153,11 @@ typedef struct {
   uint64_t word_count;           /* d_words must hold word_count words (mult. of 256)   */
   uint64_t out_lo, out_hi;       /* this plan writes symbols [out_lo, out_hi)            */
   uint64_t out_base;             /* d_out[0] is symbol out_base (out_lo & ~511)          */
-  uint64_t out_count;            /* d_out must hold out_count (>= out_hi - out_base) bytes */
+  uint64_t out_count;            /* d_out must hold out_count (>= out_hi - out_base) symbols */
   uint64_t workspace_bytes;      /* d_workspace size (LUT + task table + status)       */
   uint64_t upload_bytes;         /* bytes recoil_decoder_upload copies host->device     */
+  uint32_t symbol_bytes;         /* 1 (8-bit symbols) or 2 (adaptive "RCA1", uint16_t)   */
+  uint32_t n_models;             /* adaptive: K models; else 1                          */
 } recoil_plan;
 
 /* Host half of the path (DESIGN.md row a1): parse the container
@@ -176,10 +199,26 @@ int recoil_decoder_launches(const recoil_decoder *dec);
 
 void recoil_decoder_destroy(recoil_decoder *dec);
 
+/* Adaptive decode ("RCA1" containers; NEXT rows 1 + 4 of SURVEY.md §8(f)):
+ * symbol i was coded with model d_model_ids[i] (P:227 item (3): "the
+ * probability distribution used in every iteration is dynamic, determined
+ * using symbol index as a key"), 16-bit symbols.  d_model_ids: device,
+ * one byte per symbol of the WHOLE stream (indexed from symbol 0, 16-byte
+ * aligned; ids >= K are clamped).  d_out: uint16_t symbols, d_out[i - out_base]
+ * (plan.symbol_bytes = 2).  Otherwise as recoil_decode.  The model tables go
+ * to shared memory: E_UNSUPPORTED if they exceed it (more than 65535 table
+ * entries in total, or too large for one block).  Errors: E_ARG (static
+ * container, misaligned ids), E_CUDA, E_UNSUPPORTED. */
+int recoil_decode_adaptive(recoil_decoder *dec, void *d_workspace, const uint16_t *d_words,
+                           const uint8_t *d_model_ids, uint16_t *d_out, void *cuda_stream);
+
 /* Resident warps per SM of the decode kernel on `device` and the SM count
  * (cudaOccupancyMaxActiveBlocksPerMultiprocessor): the split count
  * that fills the GPU is warps_per_sm * sm_count * waves. */
 int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);  /* 1 <= n <= 16 */
+/* The same for the adaptive kernel with table_bytes of model tables
+ * (4 (64 K + E + K) bytes for K models with E table entries). */
+int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes, int *warps_per_sm, int *sm_count);
 
 /* ---------------------------------------------------------------------- */
 /* End-to-end pipelined decode on one GPU (host container -> host symbols)  */

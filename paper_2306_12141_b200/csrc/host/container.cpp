@@ -111,6 +111,36 @@ int parse_model(const uint8_t *c, uint64_t len, uint64_t *pos, uint32_t n, uint3
   return sum == (1ull << n) ? RECOIL_OK : RECOIL_E_INCONSISTENT;
 }
 
+// Adaptive model block ("RCA1"): u32 K, K x (u32 base, u32 len), sum(len) x u32 f;
+// every model sums to 2^n and stays inside the 16-bit symbol range.
+int parse_models(const uint8_t *c, uint64_t len, uint64_t *pos, Container *o) {
+  if (*pos + 4 > len) return RECOIL_E_TRUNCATED;
+  o->K = (uint32_t)get_le(c + *pos, 4);
+  *pos += 4;
+  if (o->K < 1 || o->K > 256) return RECOIL_E_INCONSISTENT;
+  if (*pos + 8ull * o->K > len) return RECOIL_E_TRUNCATED;
+  o->mbase.resize(o->K);
+  o->mlen.resize(o->K);
+  uint64_t msum = 0;
+  for (uint32_t k = 0; k < o->K; ++k, *pos += 8) {
+    o->mbase[k] = (uint32_t)get_le(c + *pos, 4);
+    o->mlen[k] = (uint32_t)get_le(c + *pos + 4, 4);
+    if (o->mlen[k] < 1 || (uint64_t)o->mbase[k] + o->mlen[k] > 65536) return RECOIL_E_INCONSISTENT;
+    msum += o->mlen[k];
+  }
+  if (*pos + 4 * msum > len) return RECOIL_E_TRUNCATED;
+  o->mf.resize(msum);
+  for (uint64_t e = 0; e < msum; ++e, *pos += 4) o->mf[e] = (uint32_t)get_le(c + *pos, 4);
+  uint64_t e0 = 0;
+  for (uint32_t k = 0; k < o->K; ++k) {
+    uint64_t sum = 0;
+    for (uint32_t j = 0; j < o->mlen[k]; ++j) sum += o->mf[e0 + j];
+    e0 += o->mlen[k];
+    if (sum != (1ull << o->n)) return RECOIL_E_INCONSISTENT;
+  }
+  return RECOIL_OK;
+}
+
 int parse_partitioned(const uint8_t *c, uint64_t len, Container *o) {
   uint64_t pos = 28;
   int rc = parse_model(c, len, &pos, o->n, o->f);
@@ -148,10 +178,12 @@ void point_span(const Container &c, uint64_t k, int64_t *sync_start, int64_t *bi
 int parse_container(const uint8_t *c, uint64_t len, Container *o, bool light) {
   if (!c || len < 28) return c ? RECOIL_E_TRUNCATED : RECOIL_E_ARG;
   bool part = std::memcmp(c, "RCV1", 4) == 0;
-  if (!part && std::memcmp(c, "RCL1", 4) != 0) return RECOIL_E_BAD_MAGIC;
-  if (c[4] != 1 || c[5] != 8) return RECOIL_E_VERSION;
+  bool adapt = std::memcmp(c, "RCA1", 4) == 0;
+  if (!part && !adapt && std::memcmp(c, "RCL1", 4) != 0) return RECOIL_E_BAD_MAGIC;
+  if (c[4] != 1 || c[5] != (adapt ? 16 : 8)) return RECOIL_E_VERSION;
   *o = Container();
   o->partitioned = part;
+  o->adaptive = adapt;
   o->bytes = c;
   o->n = c[6];
   o->W = c[7];
@@ -171,7 +203,7 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o, bool light) {
     return rc;
   }
   uint64_t pos = 28;
-  int rc = parse_model(c, len, &pos, o->n, o->f);
+  int rc = adapt ? parse_models(c, len, &pos, o) : parse_model(c, len, &pos, o->n, o->f);
   if (rc) return rc;
   o->header_bytes = pos;
   const uint32_t W = o->W;
@@ -293,6 +325,7 @@ int write_recoil_container(const Container &c, const uint8_t *words, uint8_t *ou
   const uint64_t P = M - 1;
   uint32_t count = 0;
   for (int s = 0; s < 256; ++s) count += c.f[s] ? 1 : 0;
+  const uint64_t model_bytes = c.adaptive ? 4 + 8ull * c.K + 4ull * c.mf.size() : 2 + 5ull * count;
   std::vector<int64_t> doff(P + 1), dg(P + 1);
   uint64_t Eb = ceil_div(c.B, M), Eg = ceil_div(c.G, M);
   for (uint64_t k = 1; k <= P; ++k) {
@@ -310,7 +343,7 @@ int write_recoil_container(const Container &c, const uint8_t *words, uint8_t *ou
     pw[k] = (uint8_t)w;
     pbytes += 2ull * W + (4 + (uint64_t)W * w + 7) / 8;
   }
-  uint64_t total = 28 + 2 + 5ull * count + 4ull * W + (gbits + 7) / 8 + pbytes + 2 * c.B;
+  uint64_t total = 28 + model_bytes + 4ull * W + (gbits + 7) / 8 + pbytes + 2 * c.B;
   if (!out) {
     *len = total;
     return RECOIL_OK;
@@ -322,23 +355,33 @@ int write_recoil_container(const Container &c, const uint8_t *words, uint8_t *ou
   uint64_t meta_end = total - 2 * c.B;
   std::memset(out, 0, meta_end);
   uint8_t *q = out;
-  std::memcpy(q, "RCL1", 4);
+  std::memcpy(q, c.adaptive ? "RCA1" : "RCL1", 4);
   q[4] = 1;
-  q[5] = 8;
+  q[5] = c.adaptive ? 16 : 8;
   q[6] = (uint8_t)c.n;
   q[7] = (uint8_t)W;
   put_le(q + 8, M, 4);
   put_le(q + 12, c.N, 8);
   put_le(q + 20, c.B, 8);
   q += 28;
-  put_le(q, count, 2);
-  q += 2;
-  for (int s = 0; s < 256; ++s)
-    if (c.f[s]) {
-      q[0] = (uint8_t)s;
-      put_le(q + 1, c.f[s], 4);
-      q += 5;
+  if (c.adaptive) {
+    put_le(q, c.K, 4);
+    q += 4;
+    for (uint32_t k = 0; k < c.K; ++k, q += 8) {
+      put_le(q, c.mbase[k], 4);
+      put_le(q + 4, c.mlen[k], 4);
     }
+    for (size_t e = 0; e < c.mf.size(); ++e, q += 4) put_le(q, c.mf[e], 4);
+  } else {
+    put_le(q, count, 2);
+    q += 2;
+    for (int s = 0; s < 256; ++s)
+      if (c.f[s]) {
+        q[0] = (uint8_t)s;
+        put_le(q + 1, c.f[s], 4);
+        q += 5;
+      }
+  }
   for (uint32_t j = 0; j < W; ++j, q += 4) put_le(q, c.finals[j], 4);
   BitWriter bw{q};
   put_series(&bw, doff.data(), P, true, 5);
@@ -408,6 +451,8 @@ extern "C" int recoil_inspect(const uint8_t *container, uint64_t len, recoil_inf
     info->prob_bits = c.n;
     info->lanes = c.W;
     info->partitioned = c.partitioned ? 1 : 0;
+    info->symbol_bits = c.adaptive ? 16 : 8;
+    info->n_models = c.adaptive ? c.K : 1;
     info->header_bytes = c.header_bytes;
     info->meta_bytes = c.meta_bytes;
     info->word_bytes = 2 * c.B;

@@ -192,20 +192,22 @@ class Selector {
 };
 
 // Serial 32-way interleaved encoder (Eq. 1 + Eq. 3, renormalisation outputs of
-// a group boundary in increasing lane order, initial state L).
-template <bool kLog>
-int interleaved_encode(const uint8_t *sym, uint64_t N, const SymInfo *si, uint32_t n,
-                       std::vector<uint16_t> *words, uint32_t final_states[32], Selector *sel) {
+// a group boundary in increasing lane order, initial state L).  info(i) gives
+// f, F and the Eq. 3 threshold of symbol i: the symbol's entry of the static
+// model, or of model mid[i] for the adaptive codec (P:227 item (3)).
+template <bool kLog, class Info>
+int interleaved_encode_gen(uint64_t N, const Info &info, uint32_t n, std::vector<uint16_t> *words,
+                           uint32_t final_states[32], Selector *sel) {
   uint32_t x[32];
   for (uint32_t j = 0; j < kLanes; ++j) x[j] = kL;
   for (uint64_t i = 0; i < N; ++i)
-    if (si[sym[i]].f == 0) return RECOIL_E_ZERO_FREQ;
+    if (info(i).f == 0) return RECOIL_E_ZERO_FREQ;
   uint64_t G = ceil_div(N, kLanes);
   for (uint64_t g = 0; g < G; ++g) {
     uint64_t base = g * kLanes;
     uint32_t lanes = (uint32_t)std::min<uint64_t>(kLanes, N - base);
     for (uint32_t j = 0; j < lanes; ++j) {
-      const SymInfo &s = si[sym[base + j]];
+      const SymInfo &s = info(base + j);
       if (x[j] >= s.thr) {  // single step suffices since b >= n
         if (kLog) sel->on_event(words->size(), j, (int64_t)(base + j) - (int64_t)kLanes, x[j] >> kWordBits);
         words->push_back((uint16_t)x[j]);
@@ -213,13 +215,36 @@ int interleaved_encode(const uint8_t *sym, uint64_t N, const SymInfo *si, uint32
       }
     }
     for (uint32_t j = 0; j < lanes; ++j) {
-      const SymInfo &s = si[sym[base + j]];
+      const SymInfo &s = info(base + j);
       uint32_t q = div_recip(x[j], s.rcp);
       x[j] = (q << n) + s.F + (x[j] - q * s.f);
     }
   }
   for (uint32_t j = 0; j < kLanes; ++j) final_states[j] = x[j];
   return RECOIL_OK;
+}
+
+template <bool kLog>
+int interleaved_encode(const uint8_t *sym, uint64_t N, const SymInfo *si, uint32_t n,
+                       std::vector<uint16_t> *words, uint32_t final_states[32], Selector *sel) {
+  auto info = [&](uint64_t i) -> const SymInfo & { return si[sym[i]]; };
+  return interleaved_encode_gen<kLog>(N, info, n, words, final_states, sel);
+}
+
+// Fill c's split metadata from the selector's points.
+void take_points(const Selector &sel, Container *c) {
+  size_t P = sel.points.size();
+  c->M = (uint32_t)P + 1;
+  c->offset.resize(P);
+  c->maxg.resize(P);
+  c->state.resize(P * kLanes);
+  c->gdiff.resize(P * kLanes);
+  for (size_t k = 0; k < P; ++k) {
+    c->offset[k] = sel.points[k].offset;
+    c->maxg[k] = sel.points[k].maxg;
+    std::memcpy(&c->state[k * kLanes], sel.points[k].state, 64);
+    std::memcpy(&c->gdiff[k * kLanes], sel.points[k].gdiff, 64);
+  }
 }
 
 }  // namespace
@@ -247,18 +272,63 @@ int encode_recoil(const uint8_t *sym, uint64_t N, const uint32_t freqs[256], uin
   if (rc) return rc;
   sel.finish();
   c->B = words->size();
-  size_t P = sel.points.size();
-  c->M = (uint32_t)P + 1;
-  c->offset.resize(P);
-  c->maxg.resize(P);
-  c->state.resize(P * kLanes);
-  c->gdiff.resize(P * kLanes);
-  for (size_t k = 0; k < P; ++k) {
-    c->offset[k] = sel.points[k].offset;
-    c->maxg[k] = sel.points[k].maxg;
-    std::memcpy(&c->state[k * kLanes], sel.points[k].state, 64);
-    std::memcpy(&c->gdiff[k * kLanes], sel.points[k].gdiff, 64);
+  take_points(sel, c);
+  return RECOIL_OK;
+}
+
+// Adaptive codec (index-keyed models, 16-bit symbols; P:227 item (3), P:411,
+// P:514): model k covers values base[k] .. base[k]+len[k]-1 with frequencies
+// freqs[off_k + j]; symbol i is coded with model mid[i].  Same split selector.
+int encode_recoil_adaptive(const uint16_t *sym, uint64_t N, const uint8_t *mid, uint32_t K, const uint32_t *base,
+                           const uint32_t *len, const uint32_t *freqs, uint32_t n, uint32_t M, Container *c,
+                           std::vector<uint16_t> *words) {
+  if (n < 1 || n > 16 || K < 1 || K > 256 || M < 1) return RECOIL_E_ARG;
+  std::vector<uint64_t> off(K + 1, 0);
+  for (uint32_t k = 0; k < K; ++k) {
+    if (len[k] < 1 || (uint64_t)base[k] + len[k] > 65536) return RECOIL_E_ARG;
+    off[k + 1] = off[k] + len[k];
   }
+  std::vector<SymInfo> si(off[K]);
+  for (uint32_t k = 0; k < K; ++k) {
+    uint64_t sum = 0;
+    for (uint32_t j = 0; j < len[k]; ++j) {
+      SymInfo &e = si[off[k] + j];
+      const uint32_t f = freqs[off[k] + j];
+      e.f = f;
+      e.F = (uint32_t)sum;
+      e.thr = (uint64_t)f << (32 - n);
+      if (f) e.rcp = make_recip(f);
+      sum += f;
+    }
+    if (sum != (1ull << n)) return RECOIL_E_ARG;
+  }
+  static const SymInfo kAbsent{};  // f = 0: rejected as E_ZERO_FREQ
+  for (uint64_t i = 0; i < N; ++i)
+    if (mid[i] >= K || sym[i] < base[mid[i]] || sym[i] - base[mid[i]] >= len[mid[i]]) return RECOIL_E_ZERO_FREQ;
+  auto info = [&](uint64_t i) -> const SymInfo & {
+    const uint32_t k = mid[i];
+    return (k < K) ? si[off[k] + (sym[i] - base[k])] : kAbsent;
+  };
+  words->clear();
+  words->reserve(N / 2 + 64);
+  c->partitioned = false;
+  c->adaptive = true;
+  c->n = n;
+  c->W = kLanes;
+  c->N = N;
+  c->G = ceil_div(N, kLanes);
+  c->K = K;
+  c->mbase.assign(base, base + K);
+  c->mlen.assign(len, len + K);
+  c->mf.assign(freqs, freqs + off[K]);
+  c->finals.assign(kLanes, 0);
+  Selector sel(N, M);
+  int rc = M > 1 ? interleaved_encode_gen<true>(N, info, n, words, c->finals.data(), &sel)
+                 : interleaved_encode_gen<false>(N, info, n, words, c->finals.data(), &sel);
+  if (rc) return rc;
+  sel.finish();
+  c->B = words->size();
+  take_points(sel, c);
   return RECOIL_OK;
 }
 
@@ -327,50 +397,56 @@ int encode_partitioned(const uint8_t *sym, uint64_t N, const uint32_t freqs[256]
 
 using namespace recoil;
 
-extern "C" int recoil_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]) {
-  if (!hist || !f || n < 1 || n > 16) return RECOIL_E_ARG;
+extern "C" int recoil_quantize(const uint64_t *hist, uint32_t count, uint32_t n, uint32_t *f) {
+  if (!hist || !f || count < 1 || n < 1 || n > 16) return RECOIL_E_ARG;
   uint64_t total = 0, distinct = 0, R = 1ull << n;
-  for (int s = 0; s < 256; ++s) {
+  for (uint32_t s = 0; s < count; ++s) {
     total += hist[s];
     distinct += hist[s] ? 1 : 0;
   }
   if (total == 0) return RECOIL_E_EMPTY;
   if (distinct > R) return RECOIL_E_ALPHABET;
-  // order of symbols by (remainder desc, symbol asc) for the largest-remainder pass
-  uint64_t rem[256];
-  bool raised[256];
-  uint64_t sum = 0;
-  for (int s = 0; s < 256; ++s) {
-    raised[s] = false;
-    rem[s] = 0;
-    f[s] = 0;
-    if (!hist[s]) continue;
-    unsigned __int128 prod = (unsigned __int128)hist[s] * R;
-    uint64_t q = (uint64_t)(prod / total);
-    rem[s] = (uint64_t)(prod % total);
-    if (q < 1) {
-      q = 1;
-      raised[s] = true;
+  try {
+    // order of symbols by (remainder desc, symbol asc) for the largest-remainder pass
+    std::vector<uint64_t> rem(count, 0);
+    std::vector<uint8_t> raised(count, 0);
+    uint64_t sum = 0;
+    for (uint32_t s = 0; s < count; ++s) {
+      f[s] = 0;
+      if (!hist[s]) continue;
+      unsigned __int128 prod = (unsigned __int128)hist[s] * R;
+      uint64_t q = (uint64_t)(prod / total);
+      rem[s] = (uint64_t)(prod % total);
+      if (q < 1) {
+        q = 1;
+        raised[s] = 1;
+      }
+      f[s] = (uint32_t)q;
+      sum += q;
     }
-    f[s] = (uint32_t)q;
-    sum += q;
+    if (sum < R) {
+      std::vector<uint32_t> order;
+      for (uint32_t s = 0; s < count; ++s)
+        if (hist[s] && !raised[s]) order.push_back(s);
+      std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return rem[a] > rem[b]; });
+      for (size_t i = 0; sum < R && i < order.size(); ++i, ++sum) f[order[i]]++;
+      if (sum < R) return RECOIL_E_ARG;  // unreachable (shortfall < #non-raised symbols)
+    }
+    while (sum > R) {
+      int64_t best = -1;
+      for (uint32_t s = 0; s < count; ++s)
+        if (f[s] > 1 && (best < 0 || f[s] > f[best] || (f[s] == f[best] && hist[s] < hist[best]))) best = s;
+      f[best]--;
+      sum--;
+    }
+    return RECOIL_OK;
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
   }
-  if (sum < R) {
-    int order[256], k = 0;
-    for (int s = 0; s < 256; ++s)
-      if (hist[s] && !raised[s]) order[k++] = s;
-    std::stable_sort(order, order + k, [&](int a, int b) { return rem[a] > rem[b]; });
-    for (int i = 0; sum < R && i < k; ++i, ++sum) f[order[i]]++;
-    if (sum < R) return RECOIL_E_ARG;  // unreachable (shortfall < #non-raised symbols)
-  }
-  while (sum > R) {
-    int best = -1;
-    for (int s = 0; s < 256; ++s)
-      if (f[s] > 1 && (best < 0 || f[s] > f[best] || (f[s] == f[best] && hist[s] < hist[best]))) best = s;
-    f[best]--;
-    sum--;
-  }
-  return RECOIL_OK;
+}
+
+extern "C" int recoil_build_model(const uint64_t hist[256], uint32_t n, uint32_t f[256]) {
+  return recoil_quantize(hist, 256, n, f);
 }
 
 extern "C" int recoil_encode(const uint8_t *symbols, uint64_t N, const uint32_t freqs[256],
@@ -387,6 +463,34 @@ extern "C" int recoil_encode(const uint8_t *symbols, uint64_t N, const uint32_t 
     Container c;
     std::vector<uint16_t> words;
     int rc = encode_recoil(symbols, N, freqs, n, M, &c, &words);
+    if (rc) return rc;
+    std::vector<uint8_t> wbytes(2 * words.size());
+    for (size_t i = 0; i < words.size(); ++i) {
+      wbytes[2 * i] = (uint8_t)words[i];
+      wbytes[2 * i + 1] = (uint8_t)(words[i] >> 8);
+    }
+    return write_recoil_container(c, wbytes.data(), out, len);
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}
+
+extern "C" int recoil_encode_adaptive(const uint16_t *symbols, uint64_t N, const uint8_t *model_ids,
+                                      uint32_t n_models, const uint32_t *model_base, const uint32_t *model_len,
+                                      const uint32_t *freqs, uint32_t n, uint32_t M, uint8_t *out, uint64_t *len) {
+  if (!len || !freqs || !model_base || !model_len || (N && (!symbols || !model_ids)) || M < 1 || n < 1 || n > 16 ||
+      n_models < 1 || n_models > 256)
+    return RECOIL_E_ARG;
+  if (!out) {
+    uint64_t msum = 0;
+    for (uint32_t k = 0; k < n_models; ++k) msum += model_len[k];
+    *len = 28 + 4 + 8ull * n_models + 4 * msum + 4ull * kLanes + (10 + 66ull * M) / 8 + 2 + 131ull * M + 2 * N + 64;
+    return RECOIL_OK;
+  }
+  try {
+    Container c;
+    std::vector<uint16_t> words;
+    int rc = encode_recoil_adaptive(symbols, N, model_ids, n_models, model_base, model_len, freqs, n, M, &c, &words);
     if (rc) return rc;
     std::vector<uint8_t> wbytes(2 * words.size());
     for (size_t i = 0; i < words.size(); ++i) {

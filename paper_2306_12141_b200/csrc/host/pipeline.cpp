@@ -73,6 +73,7 @@ extern "C" int recoil_pipeline_create(const uint8_t *container, uint64_t len, ui
     auto c = std::make_shared<Container>();
     int rc = parse_container(container, len, c.get(), /*light=*/true);
     if (rc) return rc;
+    if (c->adaptive) return RECOIL_E_UNSUPPORTED;  // needs the model ids (recoil_decode_adaptive)
     Pipeline *pl = new Pipeline();
     pl->bytes = container;
     pl->len = len;

@@ -41,6 +41,55 @@ void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut) {
   std::memcpy(lut->data() + ((size_t)1 << n), fF, 1024);
 }
 
+int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout, uint32_t *Eout) {
+  const uint32_t K = c.K, n = c.n;
+  // per model: entries up to the last value with f > 0 (trailing zero-f values
+  // cannot be decoded and would carry F = 2^n, which does not fit 16 bits)
+  std::vector<uint32_t> off(K + 1, 0), keep(K);
+  std::vector<uint64_t> moff(K + 1, 0);
+  for (uint32_t k = 0; k < K; ++k) {
+    moff[k + 1] = moff[k] + c.mlen[k];
+    uint32_t last = 0;
+    for (uint32_t j = 0; j < c.mlen[k]; ++j)
+      if (c.mf[moff[k] + j]) last = j;
+    keep[k] = last + 1;
+    off[k + 1] = off[k] + keep[k];
+  }
+  const uint32_t E = off[K];
+  if (E > 65535) return RECOIL_E_UNSUPPORTED;
+  const uint32_t Epad = (E + 3) & ~3u;
+  std::vector<uint32_t> w((size_t)K * 64 + Epad + K, 0);
+  uint32_t *coarse = w.data(), *ent = w.data() + (size_t)K * 64, *delta = ent + Epad;
+  const uint32_t shift = n > 6 ? n - 6 : 0, nb = 1u << (n - shift);
+  std::vector<uint32_t> F;
+  for (uint32_t k = 0; k < K; ++k) {
+    F.assign(keep[k], 0);
+    uint32_t acc = 0;
+    for (uint32_t j = 0; j < keep[k]; ++j) {
+      const uint32_t f = c.mf[moff[k] + j];
+      F[j] = acc;
+      acc += f;
+      ent[off[k] + j] = F[j] | (((f - 1) & 0xFFFFu) << 16);
+    }
+    delta[k] = c.mbase[k] - off[k];  // value = entry index + delta (mod 2^32)
+    // largest j with F_j <= slot (F non-decreasing)
+    auto entry_of = [&](uint32_t slot) {
+      uint32_t j = (uint32_t)(std::upper_bound(F.begin(), F.end(), slot) - F.begin());
+      return off[k] + (j ? j - 1 : 0);
+    };
+    for (uint32_t b = 0; b < 64; ++b) {
+      const uint32_t bb = std::min(b, nb - 1);
+      const uint32_t s0 = bb << shift, s1 = ((bb + 1) << shift) - 1;
+      coarse[k * 64 + b] = entry_of(s0) | (entry_of(s1) << 16);
+    }
+  }
+  blob->resize(4 * w.size());
+  std::memcpy(blob->data(), w.data(), blob->size());
+  *Kout = K;
+  *Eout = E;
+  return RECOIL_OK;
+}
+
 static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
@@ -56,7 +105,12 @@ int build_decoder(const uint8_t *cbytes, uint64_t len, uint64_t task_begin, uint
 static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   const Container &c = *d->c;
   d->fused = true;
-  pack_lut(c.f, c.n, &d->lut);
+  if (c.adaptive) {
+    int rc0 = pack_adaptive(c, &d->lut, &d->ad_K, &d->ad_E);
+    if (rc0) return rc0;
+  } else {
+    pack_lut(c.f, c.n, &d->lut);
+  }
   d->finals = c.finals;
   d->heads.clear();
   d->tasks.clear();
@@ -130,6 +184,8 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   }
   d->n_tasks = (uint32_t)d->heads.size();
   p.n_tasks = d->n_tasks;
+  p.symbol_bytes = c.adaptive ? 2 : 1;
+  p.n_models = c.adaptive ? c.K : 1;
   d->lut_off = 16;
   d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
@@ -145,6 +201,8 @@ int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begi
   const Container &c = *d->c;
   if (task_end > c.M) task_end = c.M;
   if (task_begin > task_end) return RECOIL_E_ARG;
+  // adaptive containers: GPU decode only (fused plan; recoil_decode_adaptive)
+  if (c.adaptive && !(for_gpu && c.light)) return RECOIL_E_UNSUPPORTED;
   {
     int present = 0;
     for (int s = 0; s < 256; ++s)
@@ -259,6 +317,8 @@ int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begi
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
   d->n_tasks = (uint32_t)d->tasks.size();
   p.workspace_bytes = align16(d->tasks_off + sizeof(TaskRec) * d->tasks.size());
+  p.symbol_bytes = 1;
+  p.n_models = 1;
   p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);
   return RECOIL_OK;
 }

@@ -46,8 +46,12 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 #ifndef RECOIL_MIN_BLOCKS
 #define RECOIL_MIN_BLOCKS 6
 #endif
+// NB = 0 is the adaptive codec (NEXT rows 1 + 4: index-keyed models, 16-bit
+// symbols, n at run time); its model tables live in dynamic shared memory.
 template <int NB>
-constexpr int min_blocks() { return NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
+__host__ __device__ constexpr int min_blocks() { return NB == 0 ? 3 : NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
+template <int NB>
+__host__ __device__ constexpr int sym_bytes() { return NB == 0 ? 2 : 1; }
 constexpr int kRingChunks = 4;
 constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
 constexpr uint32_t kRingBytes = 2 * kRingWords;
@@ -71,6 +75,10 @@ struct Params {
   // FMA pipe (IMAD) instead of the ALU pipe, which is the busiest one:
   int32_t neg2;           // -2: cursor arithmetic as IMAD instead of IADD3
   int32_t kneg4096;       // -2^12: see Warp::decode
+  // adaptive codec (NB = 0): model id of every symbol (absolute index, 16-B
+  // aligned), model count, table entries, n
+  const uint8_t *mid;
+  uint32_t ad_K, ad_E, nbits;
 };
 
 // Static shared memory per block (about 33 KB for n = 11): the word rings need
@@ -84,11 +92,12 @@ struct __align__(16) Smem {
   // base | ((x << 2) & mask).  The LUT is at least 2 KB, so the word rings
   // after it start 2 KB-aligned (ring addresses are base | (pos & 0x7FE)).
   // Both alignments are checked at kernel start.
-  uint8_t stage[kWarpsPerBlock][kBlockBytes];  // 8 x 512 B output staging
+  uint8_t stage[kWarpsPerBlock][kBlockBytes * sym_bytes<NB>()];  // 8 x 512 symbols output staging
   TaskRec rec[kWarpsPerBlock][2];              // current / next task record
   // n <= 12: packed LUT s | bias << 8 | f << 20.  n >= 13 (NEXT row 1):
   // f and F per symbol here, the 2^n slot -> symbol bytes in dynamic smem.
-  uint32_t lut[NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512];
+  // NB = 0 (adaptive): the model ids of each warp's current output block (8 x 512 B).
+  uint32_t lut[NB == 0 ? 1024 : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512];
   uint16_t ring[kWarpsPerBlock][kRingWords];   // 8 x 2 KB word windows
 };
 constexpr int kOrLutMaxBits = 11;  // LUT base alignment trick up to 8 KB
@@ -108,6 +117,17 @@ __device__ __forceinline__ int4 lds_v4(uint32_t a) {
   int4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -154,6 +174,10 @@ struct Warp {
   uint32_t ring32;   // 2 KB-aligned shared address of this warp's word ring
   uint32_t stage32;  // this warp's 512-B staging block + lane
   uint32_t lut32;    // shared address of the packed LUT (n <= 12)
+  // adaptive (NB = 0): this lane's model-id slot of the staged block, the
+  // model tables (coarse bucket -> entry range, entries F | (f-1) << 16,
+  // per-model value offset), n, the coarse shift and the largest model id
+  uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax;
   uint32_t gt;       // lanes above this one
   int lane;
   int cursor2;       // 2 x (slice-relative index of the next word to read)
@@ -195,7 +219,25 @@ struct Warp {
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
   template <int NB>
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
-    if constexpr (NB <= kNarrowMaxBits) {
+    if constexpr (NB == 0) {
+      // Eq. 2 under model mid(i) (P:227 item (3)): the entry j of the model
+      // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (64 buckets of
+      // the slot range per model) and a warp-converged binary search inside
+      // the bucket's entry range; value = j + delta(model)
+      const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
+      const uint32_t slot = x & ((1u << nb) - 1);
+      const uint32_t cb = lds_u32(coarse32 + (((km << 6) + (slot >> cshift)) << 2));
+      uint32_t lo = cb & 0xFFFFu, hi = cb >> 16;
+      while (__any_sync(kFull, lo < hi)) {
+        if (lo < hi) {
+          const uint32_t m = (lo + hi + 1) >> 1;
+          if ((lds_u32(ent32 + 4 * m) & 0xFFFFu) <= slot) lo = m; else hi = m - 1;
+        }
+      }
+      const uint32_t e = lds_u32(ent32 + 4 * lo);
+      sts_u16(stage32 + k * 64, lo + lds_u32(delta32 + 4 * km));
+      return ((e >> 16) + 1) * (x >> nb) + slot - (e & 0xFFFFu);  // f (x >> n) + slot - F
+    } else if constexpr (NB <= kNarrowMaxBits) {
       const uint32_t e = NB <= kOrLutMaxBits ? lds_u32(lut32 | ((x << 2) & ((4u << NB) - 4)))
                                              : lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
       sts_u8(stage32 + k * 32, e);
@@ -212,16 +254,20 @@ struct Warp {
   }
   // a8: write an output block: every 16-B chunk of this lane inside the task's
   // write window [woff, wend) (offsets relative to the block's base `dst`).
+  // S = symbol bytes: each lane writes 16 S bytes (its part of the 512-symbol block)
+  template <int S>
   __device__ __forceinline__ void flush_at(uint8_t *dst, int c, int woff, int wend) {
     __syncwarp();
-    if (c >= woff && c + 16 <= wend) stg_v4(dst + 16 * lane, lds_v4(stage32 + 15 * lane));
-    __syncwarp();
-  }
-  __device__ __forceinline__ void flush(uint8_t *dst, int rel, int woff, int wend) {
-    __syncwarp();
-    const int c = rel + 16 * lane;
-    if (c >= woff && c + 16 <= wend) stg_v4(dst + 16 * lane, lds_v4(stage32 + 15 * lane));
+    if (c >= woff && c + 16 * S <= wend) {
+      const uint32_t a = stage32 + (16 * S - S) * lane;  // staging base + 16 S lane
+      stg_v4(dst + 16 * S * lane, lds_v4(a));
+      if (S == 2) stg_v4(dst + 32 * lane + 16, lds_v4(a + 16));
+    }
     __syncwarp();  // the staging block is rewritten by the next group steps
+  }
+  template <int S>
+  __device__ __forceinline__ void flush(uint8_t *dst, int rel, int woff, int wend) {
+    flush_at<S>(dst, rel + 16 * S * lane, woff, wend);
   }
 };
 
@@ -287,8 +333,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   __shared__ Smem<NB> sm;
   extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
 
+  constexpr int S = sym_bytes<NB>();
   // a2: stage the LUT in shared memory (per block)
-  if constexpr (NB <= kNarrowMaxBits) {
+  if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
+    const uint32_t words = p.ad_K * 64 + ((p.ad_E + 3) & ~3u) + p.ad_K;
+    for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
+      reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+    for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
+      reinterpret_cast<uint32_t *>(sym_dyn)[i] = reinterpret_cast<const uint32_t *>(p.lut)[i];
+  } else if constexpr (NB <= kNarrowMaxBits) {
     constexpr uint32_t kWords = 1u << NB;
     if (kWords >= 4) {
       for (uint32_t i = threadIdx.x; i < kWords / 4; i += kThreads)
@@ -309,10 +362,19 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   const int lane = w.lane;
   const int warp = threadIdx.x >> 5;
   w.ring32 = smem_addr(&sm.ring[warp][0]);
-  w.stage32 = smem_addr(&sm.stage[warp][lane]);
+  w.stage32 = smem_addr(&sm.stage[warp][S * lane]);
   w.gt = lanemask_gt();
   w.lut32 = smem_addr(sm.lut);
-  if ((NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
+  if constexpr (NB == 0) {
+    w.mid32 = w.lut32 + 512 * warp + lane;
+    w.coarse32 = smem_addr(sym_dyn);
+    w.ent32 = w.coarse32 + 256 * p.ad_K;
+    w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
+    w.nb = p.nbits;
+    w.cshift = p.nbits > 6 ? p.nbits - 6 : 0;
+    w.kmax = p.ad_K - 1;
+  }
+  if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
     // shared-memory layout assumption broken: fail loudly
     if (threadIdx.x == 0) atomicOr(&p.status->flags, 4u);
     return;
@@ -467,11 +529,40 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) min_init = min(min_init, __shfl_xor_sync(kFull, min_init, o));
     const int32_t g_sync_end = max(min_init, lo_group);
-    // 32-bit output bookkeeping relative to the block of lo_group
+    // 32-bit output bookkeeping relative to the block of lo_group (bytes: S per symbol)
     const int32_t b_lo = lo_group >> 4;
-    uint8_t *const out_blo = p.out + ((uint64_t)b_lo * kBlockBytes - p.out_base);
-    const int woff = lo_group * (int)kLanes - b_lo * (int)kBlockBytes;  // 0..511
-    const int wend = (int)(whi - (uint64_t)b_lo * kBlockBytes);
+    uint8_t *const out_blo = p.out + ((uint64_t)b_lo * kBlockBytes - p.out_base) * S;
+    const int woff = (lo_group * (int)kLanes - b_lo * (int)kBlockBytes) * S;  // 0..511 symbols
+    const int wend = (int)(whi - (uint64_t)b_lo * kBlockBytes) * S;
+    constexpr int kBlk = (int)kBlockBytes * S;  // output block bytes
+
+    // adaptive: the model ids of the block being decoded are staged in shared
+    // memory (16 B per lane); the next lower block's ids are loaded into
+    // registers meanwhile (one block of look-ahead)
+    uint4 midv = make_uint4(0, 0, 0, 0);
+    int mid_blk = -1;
+    auto mid_load = [&](int blk) -> uint4 {
+      const uint64_t N = ((uint64_t)p.N_hi << 32) | p.N_lo;
+      const uint64_t i0 = (uint64_t)blk * kBlockBytes + 16 * lane;
+      if (i0 + 16 <= N) return __ldg(reinterpret_cast<const uint4 *>(p.mid + i0));
+      uint32_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if (i0 + b < N) v[b >> 2] |= (uint32_t)p.mid[i0 + b] << (8 * (b & 3));
+      return make_uint4(v[0], v[1], v[2], v[3]);
+    };
+    auto stage_block = [&](int blk) {
+      if constexpr (NB == 0) {
+        const uint4 v = (mid_blk == blk) ? midv : mid_load(blk);
+        __syncwarp();
+        sts_v4(w.mid32 - lane + 16 * lane, v);
+        __syncwarp();
+        if (blk > 0) {
+          midv = mid_load(blk - 1);
+          mid_blk = blk - 1;
+        }
+      }
+    };
 
     uint32_t x = 0xFFFFFFFFu;  // uninitialised: never < L
     int32_t g = start_group;
@@ -479,19 +570,21 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     // a4: Synchronization Phase -- groups where some lane is still uninitialised
     while (g >= g_sync_end) {
       const int gb = g & ~15, ge = max(gb, g_sync_end);
+      if ((g & 15) == 15 || g == start_group) stage_block(g >> 4);
       x = run_part<NB, true>(w, lut, sym, x, g, ge, init_group, state);
       if (ge == gb) {
         const int rel = (gb >> 4) - b_lo;
-        w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
+        w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
       }
       g = ge - 1;
     }
     // a5 + a6: Decoding Phase and Cross-Boundary Phase (all lanes initialised)
     if (g >= lo_group && (g & 15) != 15) {  // head: partial block
       const int gb = g & ~15, ge = max(gb, lo_group);
+      if (g == start_group) stage_block(g >> 4);  // else staged by the sync phase
       x = run_part<NB, false>(w, lut, sym, x, g, ge, 0, 0);
       const int rel = (gb >> 4) - b_lo;
-      w.flush(out_blo + rel * (int)kBlockBytes, rel * (int)kBlockBytes, woff, wend);
+      w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
       g = ge - 1;
     }
     if (g >= lo_group) {
@@ -499,24 +592,27 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       // three blocks before the end
       int rel = (g >> 4) - b_lo;
       const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      uint8_t *dst = out_blo + rel * (int)kBlockBytes;
-      int c = rel * (int)kBlockBytes + 16 * lane;  // this lane's 16-B chunk, block-relative
+      uint8_t *dst = out_blo + rel * kBlk;
+      int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
       for (; rel >= full_lo + 3; --rel) {
+        stage_block(b_lo + rel);
         x = run_block<NB>(w, lut, sym, x);
-        w.flush_at(dst, c, woff, wend);
-        dst -= kBlockBytes;
-        c -= (int)kBlockBytes;
+        w.template flush_at<S>(dst, c, woff, wend);
+        dst -= kBlk;
+        c -= kBlk;
       }
       for (; rel >= full_lo; --rel) {
         next_task_step();
+        stage_block(b_lo + rel);
         x = run_block<NB>(w, lut, sym, x);
-        w.flush_at(dst, c, woff, wend);
-        dst -= kBlockBytes;
-        c -= (int)kBlockBytes;
+        w.template flush_at<S>(dst, c, woff, wend);
+        dst -= kBlk;
+        c -= kBlk;
       }
       if (full_lo) {  // tail: the partial block of lo_group
+        stage_block(b_lo);
         x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
-        w.flush(out_blo, 0, woff, wend);
+        w.template flush<S>(out_blo, 0, woff, wend);
       }
     }
     while (next_state < 3) next_task_step();
@@ -548,7 +644,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
 }
 
 using KernelFn = void (*)(const Params);
-static KernelFn kernel_for(uint32_t nbits, bool fused) {
+static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false) {
+  if (adaptive) return fused ? recoil_decode_kernel<0, true> : nullptr;
   if (fused) switch (nbits) {
     case 1: return recoil_decode_kernel<1, true>;
     case 2: return recoil_decode_kernel<2, true>;
@@ -594,23 +691,60 @@ static KernelFn kernel_for(uint32_t nbits, bool fused) {
 static size_t smem_bytes(uint32_t nbits) {  // dynamic part only: the slot -> symbol table for n >= 13
   return nbits > (uint32_t)dev::kNarrowMaxBits ? (size_t)1 << nbits : 0;
 }
-
-static int configure(dev::KernelFn fn, uint32_t nbits) {
-  cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        (int)cudaSharedmemCarveoutMaxShared);
-  cudaError_t e2 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(nbits));
-  return (e1 == cudaSuccess && e2 == cudaSuccess) ? RECOIL_OK : RECOIL_E_CUDA;
+static size_t dyn_smem(const Decoder &d) {  // adaptive: the model tables
+  return d.c->adaptive ? d.lut.size() : smem_bytes(d.plan.prob_bits);
 }
 
-static int occupancy(uint32_t nbits, bool fused, int *blocks_per_sm) {
-  dev::KernelFn fn = dev::kernel_for(nbits, fused);
+static int occupancy(dev::KernelFn fn, size_t dyn, int *blocks_per_sm) {
   if (!fn) return RECOIL_E_ARG;
-  int rc = configure(fn, nbits);
-  if (rc) return rc;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, dev::kThreads, smem_bytes(nbits)) !=
-      cudaSuccess)
+  cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared);
+  cudaError_t e2 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return RECOIL_E_CUDA;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, dev::kThreads, dyn) != cudaSuccess)
     return RECOIL_E_CUDA;
   return RECOIL_OK;
+}
+
+static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *d_mid, uint8_t *d_out,
+                  cudaStream_t s) {
+  const recoil_plan &pl = d->plan;
+  const bool adaptive = d->c->adaptive;
+  dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive);
+  if (d->blocks_per_sm == 0) {
+    int rc = occupancy(fn, dyn_smem(*d), &d->blocks_per_sm);
+    if (rc) return rc;
+    int dev_id = 0;
+    if (cudaGetDevice(&dev_id) != cudaSuccess ||
+        cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
+      return RECOIL_E_CUDA;
+    if (d->blocks_per_sm < 1) return RECOIL_E_UNSUPPORTED;  // tables do not fit in shared memory
+  }
+  dev::Params prm;
+  prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
+  prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
+  prm.tasks = reinterpret_cast<const TaskRec *>(ws + d->tasks_off);
+  prm.heads = reinterpret_cast<const TaskHead *>(ws + d->tasks_off);
+  prm.recs = reinterpret_cast<const uint8_t *>(ws + d->rec_off);
+  prm.N_lo = (uint32_t)d->c->N;
+  prm.N_hi = (uint32_t)(d->c->N >> 32);
+  prm.G = (int32_t)d->c->G;
+  prm.status = reinterpret_cast<DeviceStatus *>(ws);
+  prm.words = d_words;
+  prm.out = d_out;
+  prm.out_base = pl.out_base;
+  prm.n_chunks = (int32_t)(pl.word_count / kChunkWords);
+  prm.n_tasks = pl.n_tasks;
+  prm.neg2 = -2;
+  prm.kneg4096 = -4096;
+  prm.mid = d_mid;
+  prm.ad_K = d->ad_K;
+  prm.ad_E = d->ad_E;
+  prm.nbits = pl.prob_bits;
+  const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
+  const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
+  fn<<<grid, dev::kThreads, dyn_smem(*d), s>>>(prm);
+  return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
 }
 
 }  // namespace recoil
@@ -658,42 +792,29 @@ extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint1
   char *ws = reinterpret_cast<char *>(d_workspace);
   if (cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return RECOIL_E_CUDA;  // status + task counter
   if (pl.n_tasks == 0) return RECOIL_OK;
+  if (d->c->adaptive) return RECOIL_E_ARG;  // needs the model ids: recoil_decode_adaptive
   if (d->single_symbol >= 0) {  // f = 2^n: every state decodes to the one symbol (Eq. 2 identity)
     return cudaMemsetAsync(d_out + (pl.out_lo - pl.out_base), d->single_symbol, pl.out_hi - pl.out_lo, s) ==
                    cudaSuccess
                ? RECOIL_OK
                : RECOIL_E_CUDA;
   }
-  if (d->blocks_per_sm == 0) {
-    int rc = occupancy(pl.prob_bits, d->fused, &d->blocks_per_sm);
-    if (rc) return rc;
-    int dev_id = 0;
-    if (cudaGetDevice(&dev_id) != cudaSuccess ||
-        cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
-      return RECOIL_E_CUDA;
-    if (d->blocks_per_sm < 1) return RECOIL_E_CUDA;
-  }
-  dev::Params prm;
-  prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
-  prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
-  prm.tasks = reinterpret_cast<const TaskRec *>(ws + d->tasks_off);
-  prm.heads = reinterpret_cast<const TaskHead *>(ws + d->tasks_off);
-  prm.recs = reinterpret_cast<const uint8_t *>(ws + d->rec_off);
-  prm.N_lo = (uint32_t)d->c->N;
-  prm.N_hi = (uint32_t)(d->c->N >> 32);
-  prm.G = (int32_t)d->c->G;
-  prm.status = reinterpret_cast<DeviceStatus *>(ws);
-  prm.words = d_words;
-  prm.out = d_out;
-  prm.out_base = pl.out_base;
-  prm.n_chunks = (int32_t)(pl.word_count / kChunkWords);
-  prm.n_tasks = pl.n_tasks;
-  prm.neg2 = -2;
-  prm.kneg4096 = -4096;
-  const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
-  const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
-  dev::kernel_for(pl.prob_bits, d->fused)<<<grid, dev::kThreads, smem_bytes(pl.prob_bits), s>>>(prm);
-  return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
+  return launch(d, ws, d_words, nullptr, d_out, s);
+}
+
+extern "C" int recoil_decode_adaptive(recoil_decoder *dec, void *d_workspace, const uint16_t *d_words,
+                                      const uint8_t *d_model_ids, uint16_t *d_out, void *stream) {
+  if (!dec || !d_workspace || !d_words) return RECOIL_E_ARG;
+  Decoder *d = reinterpret_cast<Decoder *>(dec);
+  const recoil_plan &pl = d->plan;
+  if (!d->c->adaptive) return RECOIL_E_ARG;
+  if ((!d_out || !d_model_ids) && pl.out_hi > pl.out_lo) return RECOIL_E_ARG;
+  if (reinterpret_cast<uintptr_t>(d_model_ids) & 15) return RECOIL_E_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(d_workspace);
+  if (cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return RECOIL_E_CUDA;  // status + task counter
+  if (pl.n_tasks == 0) return RECOIL_OK;
+  return launch(d, ws, d_words, d_model_ids, reinterpret_cast<uint8_t *>(d_out), s);
 }
 
 extern "C" int recoil_decoder_status(recoil_decoder *dec, const void *d_workspace, void *stream, uint64_t *bad) {
@@ -715,13 +836,29 @@ extern "C" int recoil_decoder_launches(const recoil_decoder *dec) {
   return (d->plan.n_tasks == 0 || d->single_symbol >= 0) ? 0 : 1;
 }
 
+extern "C" int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes, int *warps_per_sm,
+                                                int *sm_count) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
+  int per_sm = 0, sms = 0;
+  int rc = occupancy(dev::kernel_for(16, true, true), (size_t)table_bytes, &per_sm);
+  cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaSetDevice(prev);
+  if (rc) return rc;
+  if (e2 != cudaSuccess) return RECOIL_E_CUDA;
+  if (warps_per_sm) *warps_per_sm = per_sm * dev::kWarpsPerBlock;
+  if (sm_count) *sm_count = sms;
+  return RECOIL_OK;
+}
+
 extern "C" int recoil_decode_occupancy(int device, uint32_t nbits, int *warps_per_sm, int *sm_count) {
   if (nbits < 1 || nbits > kMaxGpuProbBits) return RECOIL_E_ARG;
   int prev = 0;
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0;
-  int rc = occupancy(nbits, true, &per_sm);
+  int rc = occupancy(dev::kernel_for(nbits, true), smem_bytes(nbits), &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;

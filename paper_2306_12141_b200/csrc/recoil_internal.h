@@ -23,9 +23,12 @@ constexpr int64_t kNoEndCheck = INT64_MIN;
 // Partitioned: M partitions (tasks), no points.
 struct Container {
   bool partitioned = false;
+  bool adaptive = false;          // "RCA1": 16-bit symbols, index-keyed model set (P:227 (3))
   uint32_t n = 0, W = 0, M = 0;
   uint64_t N = 0, B = 0, G = 0;
-  uint32_t f[256] = {0};
+  uint32_t f[256] = {0};          // static model ("RCL1" / "RCV1")
+  uint32_t K = 0;                 // adaptive: model k = values mbase[k] .. + mlen[k] - 1,
+  std::vector<uint32_t> mbase, mlen, mf;  // frequencies mf[off_k + j] (sum 2^n each)
   std::vector<uint32_t> finals;   // Recoil: W final states; partitioned: M x W
   std::vector<uint64_t> offset;   // Recoil: M-1 split offsets (word index of the boundary event)
   std::vector<uint64_t> maxg;     // Recoil: M-1 anchor (max) group IDs
@@ -108,6 +111,7 @@ struct Decoder {
   uint64_t lut_off = 0, finals_off = 0, tasks_off = 0, rec_off = 0;  // workspace byte offsets
   uint32_t n_tasks = 0;
   int single_symbol = -1;          // >= 0: the model has one symbol (f = 2^n): decode = fill
+  uint32_t ad_K = 0, ad_E = 0;     // adaptive: models, table entries (lut = coarse | entries | offsets)
   int blocks_per_sm = 0, sm_count = 0;  // launch geometry (occupancy API), cached
 };
 
@@ -121,6 +125,10 @@ void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
 void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,
                         uint64_t *bounds);
 void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
+// Adaptive model tables for the GPU: K x 64 coarse
+// buckets (lo | hi << 16 entry range), E entries F | (f-1) << 16 (padded to 4),
+// K value offsets.  E_UNSUPPORTED if E > 65535.
+int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
 
 
 }  // namespace recoil

@@ -33,7 +33,8 @@ EXPORTS = [
     "recoil_decode", "recoil_decoder_status", "recoil_decoder_launches", "recoil_decoder_destroy",
     "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu", "recoil_decode_cpu_ex", "recoil_cpu_simd",
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
-    "recoil_pipeline_launches", "recoil_pipeline_destroy",
+    "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
+    "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive",
 ]
 
 
@@ -48,7 +49,8 @@ class recoil_info(ctypes.Structure):
     _fields_ = [("n_symbols", ctypes.c_uint64), ("n_words", ctypes.c_uint64), ("n_splits", ctypes.c_uint32),
                 ("prob_bits", ctypes.c_uint32), ("lanes", ctypes.c_uint32), ("partitioned", ctypes.c_uint32),
                 ("header_bytes", ctypes.c_uint64), ("meta_bytes", ctypes.c_uint64),
-                ("word_bytes", ctypes.c_uint64), ("total_bytes", ctypes.c_uint64)]
+                ("word_bytes", ctypes.c_uint64), ("total_bytes", ctypes.c_uint64),
+                ("symbol_bits", ctypes.c_uint32), ("n_models", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -59,7 +61,7 @@ class recoil_plan(ctypes.Structure):
                 ("prob_bits", ctypes.c_uint32), ("word_lo", ctypes.c_uint64), ("word_count", ctypes.c_uint64),
                 ("out_lo", ctypes.c_uint64), ("out_hi", ctypes.c_uint64), ("out_base", ctypes.c_uint64),
                 ("out_count", ctypes.c_uint64), ("workspace_bytes", ctypes.c_uint64),
-                ("upload_bytes", ctypes.c_uint64)]
+                ("upload_bytes", ctypes.c_uint64), ("symbol_bytes", ctypes.c_uint32), ("n_models", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -99,6 +101,10 @@ def load(path: str = LIB_PATH):
         "recoil_pipeline_status": (i32, [P, P, u32, P]),
         "recoil_pipeline_launches": (i32, [P]),
         "recoil_pipeline_destroy": (None, [P]),
+        "recoil_quantize": (i32, [P, u32, u32, P]),
+        "recoil_encode_adaptive": (i32, [P, u64, P, u32, P, P, P, u32, u32, P, P]),
+        "recoil_decode_adaptive": (i32, [P, P, P, P, P, P]),
+        "recoil_decode_occupancy_adaptive": (i32, [i32, u64, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +260,36 @@ def recoil_decoder_destroy(handle) -> None:
         load().recoil_decoder_destroy(handle)
 
 
+def recoil_quantize(hist, prob_bits: int) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.uint64))
+    f = np.zeros(h.size, dtype=np.uint32)
+    _check(load().recoil_quantize(h.ctypes.data, h.size, prob_bits, f.ctypes.data), "recoil_quantize")
+    return f
+
+
+def recoil_encode_adaptive(symbols, model_ids, models, prob_bits: int, n_splits: int) -> np.ndarray:
+    """models: {"base": u32[K], "len": u32[K], "f": u32[sum len]}"""
+    s = np.ascontiguousarray(np.asarray(symbols, dtype=np.uint16))
+    m = np.ascontiguousarray(np.asarray(model_ids, dtype=np.uint8))
+    base = np.ascontiguousarray(np.asarray(models["base"], dtype=np.uint32))
+    ln = np.ascontiguousarray(np.asarray(models["len"], dtype=np.uint32))
+    f = np.ascontiguousarray(np.asarray(models["f"], dtype=np.uint32))
+    return _sized(load().recoil_encode_adaptive, "recoil_encode_adaptive", _ptr(s), s.size, _ptr(m), base.size,
+                  base.ctypes.data, ln.ctypes.data, f.ctypes.data, prob_bits, n_splits)
+
+
+def recoil_decode_adaptive(handle, d_workspace: int, d_words: int, d_model_ids: int, d_out: int, stream: int) -> None:
+    _check(load().recoil_decode_adaptive(handle, d_workspace, d_words, d_model_ids, d_out, stream),
+           "recoil_decode_adaptive")
+
+
+def recoil_decode_occupancy_adaptive(device: int, table_bytes: int) -> tuple[int, int]:
+    w, s = ctypes.c_int(0), ctypes.c_int(0)
+    _check(load().recoil_decode_occupancy_adaptive(device, table_bytes, ctypes.byref(w), ctypes.byref(s)),
+           "recoil_decode_occupancy_adaptive")
+    return w.value, s.value
+
+
 class GpuDecoder:
     """Owns a decoder handle plus the torch device buffers of its plan.
 
@@ -271,7 +307,20 @@ class GpuDecoder:
         self.stream = stream or torch.cuda.current_stream(self.device)
         self.workspace = torch.empty(max(p["workspace_bytes"], 16), dtype=torch.uint8, device=self.device)
         self.words = torch.empty(max(p["word_count"], 1), dtype=torch.int16, device=self.device)
-        self.out = torch.empty(max(p["out_count"], 16), dtype=torch.uint8, device=self.device)
+        self.adaptive = p["symbol_bytes"] == 2
+        self.out = torch.empty(max(p["out_count"], 16), dtype=torch.int16 if self.adaptive else torch.uint8,
+                               device=self.device)
+        self.model_ids = None  # adaptive: device tensor of the stream's model ids (set_model_ids)
+
+    def set_model_ids(self, model_ids) -> None:
+        """Adaptive containers: the model id of every symbol of the stream (host or device)."""
+        import torch
+        t = torch.as_tensor(np.ascontiguousarray(model_ids, dtype=np.uint8)) if not torch.is_tensor(model_ids) \
+            else model_ids
+        n = t.numel()
+        buf = torch.zeros(((n + 15) // 16) * 16 + 16, dtype=torch.uint8, device=self.device)
+        buf[:n].copy_(t.reshape(-1).to(torch.uint8), non_blocking=False)
+        self.model_ids = buf
 
     @property
     def stream_handle(self) -> int:
@@ -282,6 +331,12 @@ class GpuDecoder:
 
     def decode(self, out=None) -> None:
         o = self.out if out is None else out
+        if self.adaptive:
+            if self.model_ids is None:
+                raise RuntimeError("adaptive container: call set_model_ids first")
+            recoil_decode_adaptive(self.handle, self.workspace.data_ptr(), self.words.data_ptr(),
+                                   self.model_ids.data_ptr(), o.data_ptr(), self.stream_handle)
+            return
         recoil_decode(self.handle, self.workspace.data_ptr(), self.words.data_ptr(), o.data_ptr(),
                       self.stream_handle)
 

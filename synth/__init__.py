@@ -231,7 +231,7 @@ def latent_model_ids(n: int, seed: int, K: int = LATENT_K) -> np.ndarray:
     x = i % LATENT_W
     tile = ch * (plane // 64) + (y // 8) * (LATENT_W // 8) + (x // 8)
     n_ch = int(ch[-1]) + 1 if n else 0
-    n_tile = int(tile[-1]) + 1 if n else 0
+    n_tile = int(tile.max()) + 1 if n else 0
     uc = u64(n_ch, seed ^ 0xA5A5A5A5) if n else np.zeros(0, np.uint64)
     ut = u64(n_tile, seed ^ 0x5A5A5A5A) if n else np.zeros(0, np.uint64)
     a = np.floor(K * np.sqrt((uc >> np.uint64(11)).astype(np.float64) / float(1 << 53))).astype(np.int64)

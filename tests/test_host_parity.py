@@ -259,3 +259,71 @@ def test_avx512_cpu_decoder_edges_and_corruption():
         except R.RecoilError as e:
             errs.append(("err", e.rc))
     assert errs[0] == errs[1]  # same verdict from both decoders
+
+
+def _ad_random_models(rng, n, K, max_len=300):
+    base, ln, fs = [], [], []
+    for _ in range(K):
+        length = int(rng.integers(1, min(max_len, 1 << n) + 1))
+        b = int(rng.integers(0, 65536 - length + 1))
+        hist = rng.integers(1, 10 ** int(rng.integers(1, 6)), size=length).astype(np.uint64)
+        hist[rng.random(length) < 0.2] = 0
+        if not hist.any():
+            hist[0] = 1
+        base.append(b)
+        ln.append(length)
+        fs.append(oracle.quantize(hist, n))
+    return {"base": np.array(base, np.uint32), "len": np.array(ln, np.uint32), "f": np.concatenate(fs)}
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_adaptive_container_byte_identical_to_oracle(seed):
+    """NEXT rows 1 + 4: adaptive (index-keyed models, 16-bit symbols) containers == the oracle's."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([1, 3, 8, 11, 12, 16]))
+    K = int(rng.integers(1, 12))
+    models = _ad_random_models(rng, n, K)
+    N = int(rng.choice([0, 1, 31, 33, 1000, 70000]))
+    mid = rng.integers(0, K, size=N).astype(np.uint8)
+    off = np.concatenate([[0], np.cumsum(models["len"].astype(np.int64))])
+    sym = np.zeros(N, np.uint16)
+    for k in range(K):
+        sel = np.nonzero(mid == k)[0]
+        if sel.size:
+            f = models["f"][off[k]:off[k + 1]].astype(np.float64)
+            sym[sel] = models["base"][k] + rng.choice(len(f), size=sel.size, p=f / f.sum())
+    for M in (1, 5, 77):
+        c = R.recoil_encode_adaptive(sym, mid, models, n, M)
+        assert c.tobytes() == oracle.ad_recoil_encode(sym, mid, models, n, M)
+        info = R.recoil_inspect(c)
+        assert info["symbol_bits"] == 16 and info["n_models"] == K and info["n_symbols"] == N
+        for target in (2, 1):
+            assert R.recoil_combine_splits(c, target).tobytes() == oracle.combine(c.tobytes(), target)
+
+
+def test_adaptive_quantize_and_errors():
+    rng = np.random.default_rng(2)
+    for _ in range(30):
+        count = int(rng.integers(1, 3000))
+        n = int(rng.integers(max(1, int(np.ceil(np.log2(count + 1)))), 17)) if count < 65536 else 16
+        hist = rng.integers(0, 1000, size=count).astype(np.uint64)
+        if not hist.any():
+            hist[0] = 1
+        if (hist > 0).sum() > (1 << n):
+            continue
+        assert (R.recoil_quantize(hist, n) == oracle.quantize(hist, n)).all()
+    models = {"base": [100], "len": [4], "f": oracle.quantize(np.array([1, 2, 3, 0], np.uint64), 11)}
+    sym = np.array([100, 101, 102], np.uint16)
+    mid = np.zeros(3, np.uint8)
+    R.recoil_encode_adaptive(sym, mid, models, 11, 1)
+    for bad in (np.array([100, 103, 102], np.uint16), np.array([99, 100, 101], np.uint16)):
+        with pytest.raises(R.RecoilError) as e:
+            R.recoil_encode_adaptive(bad, mid, models, 11, 1)
+        assert e.value.rc == R.RECOIL_E_ZERO_FREQ
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_encode_adaptive(sym, np.array([0, 1, 0], np.uint8), models, 11, 1)
+    assert e.value.rc == R.RECOIL_E_ZERO_FREQ
+    c = R.recoil_encode_adaptive(sym, mid, models, 11, 1)
+    with pytest.raises(R.RecoilError) as e:
+        R.recoil_decode_cpu(c)
+    assert e.value.rc == R.RECOIL_E_UNSUPPORTED
