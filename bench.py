@@ -154,6 +154,46 @@ def cpu_oracle_decode_rate(container: np.ndarray, sample_tasks: int | None, reps
     return nsym / best / 1e9, nsym, best, f"oracle or_recoil_decode_tasks on {len(tasks)} of {M} tasks ({nsym} symbols)"
 
 
+def peak_hbm() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") or 6650.0)
+    except Exception:
+        return 6650.0
+
+
+def adaptive_extra(args, local, stream, timed_decode, peak):
+    """NEXT rows 1 + 4: the adaptive codec (index-keyed Gaussian models, 16-bit symbols, n = 16) on the
+    latent workload, 2^25 symbols, one split per resident warp."""
+    import synth
+    from paper_2306_12141_b200 import recoil as R
+    N = 1 << 25
+    sym, mid, h = synth.latent_workload(N, synth.seed_for(6))
+    f = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
+    models = {"base": h["base"], "len": h["len"], "f": f}
+    table_bytes = 4 * (64 * len(h["len"]) + ((int(f.size) + 3) & ~3) + len(h["len"]))
+    warps, sms = R.recoil_decode_occupancy_adaptive(local, table_bytes)
+    c = R.recoil_encode_adaptive(sym, mid, models, 16, warps * sms)
+    info = R.recoil_inspect(c)
+    dec = R.GpuDecoder(c, local, stream=stream)
+    dec.set_model_ids(mid)
+    dec.upload()
+    dec.decode()
+    rc, _ = dec.status()
+    ok = rc == 0 and bool((dec.output().cpu().numpy().view(np.uint16) == sym).all())
+    t = timed_decode(dec, args.steps, args.warmup)
+    ms = float(np.mean(t))
+    alg = 2 * N + N + 2 * info["n_words"] + dec.plan["workspace_bytes"]  # symbols out + model ids + words
+    dec.close()
+    return {"value": round(2 * N / (ms / 1e3) / 1e9, 2), "unit": "GB/s (16-bit symbols written)",
+            "symbols_per_s": round(N / (ms / 1e3), 1), "ms_per_step": round(ms, 4), "bit_exact": ok,
+            "n_symbols": N, "splits": info["n_splits"], "models": len(h["len"]), "prob_bits": 16,
+            "bits_per_symbol": round(8 * len(c) / N, 3), "resident_warps_per_sm": warps,
+            "roofline": {"bound": "hbm", "achieved": round(alg / (ms / 1e3) / 1e9, 1), "peak": peak,
+                         "frac": round(alg / (ms / 1e3) / 1e9 / peak, 4)},
+            "note": "recoil_decode_adaptive: per symbol a model id (u8) keys one of 64 discretised Gaussians "
+                    "(P:227 (3), P:514); coarse bucket + binary search in shared-memory model tables"}
+
+
 def run_reference(args, rank, world):
     """Reference arm of this tier: the oracle as it stands, on the host cores."""
     if rank != 0:
@@ -199,6 +239,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-adaptive", action="store_true", help="skip the adaptive-codec extra")
     ap.add_argument("--waves", type=int, default=0,
                     help="splits per GPU = waves x resident warps; 0 = per-config default (config2: 1, one split "
                          "per resident warp, the decoder-adaptive choice of P:84; configs 3/5: 2, measured best for "
@@ -374,6 +415,8 @@ def main():
             "recoil_combined_to_16": {"bytes": int(len(small)), "overhead_bytes": int(len(small) - len(c1))},
         }
         pdec.close()
+        if world == 1 and not args.no_adaptive:
+            extra["adaptive_latent"] = adaptive_extra(args, local, stream, timed_decode, peak_hbm())
     cpu = None
     if rank == 0 and not args.no_cpu:
         gbs, nsym, dt, desc = cpu_oracle_decode_rate(c, None if N_total <= (256 << 20) else 256, reps=1)
