@@ -79,6 +79,9 @@ struct Params {
   // aligned), model count, table entries, n
   const uint8_t *mid;
   uint32_t ad_K, ad_E, nbits;
+  // fused plans: per-task claim words (atomicMax with the decode's epoch)
+  uint32_t *claims;
+  uint32_t epoch;
 };
 
 // Static shared memory per block (about 33 KB for n = 11): the word rings need
@@ -416,14 +419,52 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       pf_pr = (flags & kHeadFirst) ? 0u : ld_win(p.recs + ((rec_prev + 64) & ~3u), lane);
     }
   };
-  uint32_t t = blockIdx.x * kWarpsPerBlock + warp;
+  // Fused plans (Recoil): chained tasks with work stealing.  A warp that
+  // finishes task t is synchronised and simply keeps decoding into task t-1
+  // (no Synchronization Phase: the Cross-Boundary Phase of P:314 extended over
+  // whole tasks) if it can claim t-1; claims are atomicMax of the decode's
+  // epoch into a per-task word.  Warp gw starts at the top of its segment of
+  // seg = ceil(tasks / warps) tasks; a warp whose chain runs into a claimed task
+  // steals an entry point: candidates are the segment midpoints, then the
+  // quarter points, ... (level-major over all segments), so a fast warp
+  // splits the largest unclaimed runs of slow warps.  Every task is decoded
+  // exactly once; a Synchronization Phase runs only at entry points.
+  const uint32_t n_tasks = p.n_tasks;
+  const uint32_t Wg = gridDim.x * kWarpsPerBlock;
+  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
+  const uint32_t seg = FUSED ? max(1u, (n_tasks + Wg - 1) / Wg) : 1u;
+  uint32_t levels = 0;
+  while ((seg >> (levels + 1)) > 0) ++levels;
+  auto claim = [&](uint32_t t) -> bool {  // warp-uniform
+    uint32_t old = 0;
+    if (lane == 0) old = atomicMax(&p.claims[t], p.epoch);
+    return __shfl_sync(kFull, old, 0) < p.epoch;
+  };
+  auto steal = [&]() -> uint32_t {  // next entry point, or n_tasks
+    for (;;) {
+      uint32_t k = 0;
+      if (lane == 0) k = atomicAdd(&p.status->next_task, 1u);
+      k = __shfl_sync(kFull, k, 0);
+      if (k >= Wg * levels) return n_tasks;
+      const uint32_t g = k % Wg, o = seg >> (k / Wg + 1);
+      const uint32_t t = g * seg + o - 1;
+      if (t < n_tasks && claim(t)) return t;
+    }
+  };
+  uint32_t t;
+  if constexpr (FUSED) {
+    t = gw * seg < n_tasks ? min(n_tasks, (gw + 1) * seg) - 1 : n_tasks;
+    if (t < n_tasks && !claim(t)) t = steal();
+  } else {
+    t = gw;
+  }
   int buf = 0;
-  if (t < p.n_tasks) {
+  if (t < n_tasks) {
     issue_task(t, 0);
     load_head(t);
     load_windows();
   }
-  while (t < p.n_tasks) {
+  while (t < n_tasks) {
     cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
     int32_t start_group, init_group, cursor0;
@@ -514,6 +555,31 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       }
     };
 
+    // fused: continuation into task t_cur - 1.  0 = not asked, 1 = claim atomic
+    // in flight, 2 = head in flight, 3 = record window in flight
+    uint32_t t_cur = t, c_old = 0;
+    int cstate = 0;
+    bool cgot = false;
+    auto chain_step = [&]() {
+      if (cstate == 0) {
+        if (lane == 0 && t_cur > 0) c_old = atomicMax(&p.claims[t_cur - 1], p.epoch);
+        cstate = 1;
+      } else if (cstate == 1) {
+        cgot = t_cur > 0 && __shfl_sync(kFull, c_old, 0) < p.epoch;
+        if (cgot) load_head(t_cur - 1);
+        cstate = 2;
+      } else if (cstate == 2) {
+        if (cgot) {
+          const uint32_t rec_prev = __shfl_sync(kFull, hw, 3), flags = __shfl_sync(kFull, hw, 5);
+          pf_pr = (flags & kHeadFirst) ? 0u : ld_win(p.recs + ((rec_prev + 64) & ~3u), lane);
+        }
+        cstate = 3;
+      }
+    };
+    auto tail_step = [&]() {
+      if constexpr (FUSED) chain_step(); else next_task_step();
+    };
+
     // a7: word window -- chunks c, c-1, c-2 resident, c-3 in flight
     w.cursor2 = 2 * cursor0;
     w.cchunk = cursor0 >> 8;
@@ -587,35 +653,88 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
       g = ge - 1;
     }
-    if (g >= lo_group) {
-      // whole blocks above the block of lo_group; the next task id is requested
-      // three blocks before the end
-      int rel = (g >> 4) - b_lo;
-      const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      uint8_t *dst = out_blo + rel * kBlk;
-      int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
-      for (; rel >= full_lo + 3; --rel) {
-        stage_block(b_lo + rel);
-        x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
-        dst -= kBlk;
-        c -= kBlk;
+    // all lanes initialised before the task's range ends (always, by Z9): only
+    // then may the warp continue into the next task without a sync phase
+    const bool all_init = min_init >= lo_group;
+    int32_t lo_g = lo_group, blo = b_lo;
+    uint8_t *oblo = out_blo;
+    int wo = woff, we = wend;
+    for (;;) {
+      if (g >= lo_g) {
+        // whole blocks above the block of lo_g; the continuation (fused) or the
+        // next task id is requested three blocks before the end
+        int rel = (g >> 4) - blo;
+        const int full_lo = ((lo_g & 15) == 0) ? 0 : 1;
+        uint8_t *dst = oblo + rel * kBlk;
+        int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
+        for (; rel >= full_lo + 3; --rel) {
+          stage_block(blo + rel);
+          x = run_block<NB>(w, lut, sym, x);
+          w.template flush_at<S>(dst, c, wo, we);
+          dst -= kBlk;
+          c -= kBlk;
+        }
+        for (; rel >= full_lo; --rel) {
+          tail_step();
+          stage_block(blo + rel);
+          x = run_block<NB>(w, lut, sym, x);
+          w.template flush_at<S>(dst, c, wo, we);
+          dst -= kBlk;
+          c -= kBlk;
+        }
+        g = (blo + full_lo) * 16 - 1;  // next group to decode
       }
-      for (; rel >= full_lo; --rel) {
-        next_task_step();
-        stage_block(b_lo + rel);
-        x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
-        dst -= kBlk;
-        c -= kBlk;
+      if constexpr (FUSED) {
+        while (cstate < 3) chain_step();
+        if (cgot && all_init) {
+          // continue into task t_cur - 1: its committed range ends where ours
+          // starts; its lower bound is the sync start of its own lower point
+          const uint32_t flags = __shfl_sync(kFull, hw, 5);
+          const uint32_t id_prev = __shfl_sync(kFull, hw, 6);
+          int64_t lo2 = 0;
+          bool bad2 = false;
+          if (!(flags & kHeadFirst)) {
+            const uint32_t rec_prev = __shfl_sync(kFull, hw, 3), maxg_prev = __shfl_sync(kFull, hw, 4);
+            uint32_t wdt;
+            const uint32_t d = series_elem(pf_pr, (rec_prev + 64) & 3u, lane, &wdt);
+            bad2 = d > maxg_prev;
+            int32_t idx = ((int32_t)maxg_prev - (int32_t)d) * 32 + lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
+            lo2 = idx;
+          }
+          bad2 |= lo2 >= (int64_t)lo;
+          if (!__any_sync(kFull, bad2)) {
+            lo = (uint64_t)lo2;
+            end_cursor = (flags & kHeadFirst) ? (int64_t)(int32_t)__shfl_sync(kFull, hw, 7) : kNoEndCheck;
+            task_id = id_prev;
+            t_cur -= 1;
+            lo_g = (int32_t)(lo >> 5);
+            blo = lo_g >> 4;
+            oblo = p.out + ((uint64_t)blo * kBlockBytes - p.out_base) * S;
+            wo = (lo_g * (int)kLanes - blo * (int)kBlockBytes) * S;
+            we = 0x7FFFFFFF;  // everything from here down lies below the entry task's write bound
+            cstate = 0;
+            cgot = false;
+            continue;
+          }
+          if (lane == 0) {  // inconsistent metadata of the next task: flag it, end the chain
+            atomicOr(&p.status->flags, 4u);
+            atomicMax(&p.status->bad_task, 0xFFFFFFFFu - id_prev);
+          }
+        }
       }
-      if (full_lo) {  // tail: the partial block of lo_group
-        stage_block(b_lo);
-        x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
-        w.template flush<S>(out_blo, 0, woff, wend);
+      if (g >= lo_g) {  // tail: the partial block of lo_g
+        stage_block(blo);
+        x = run_part<NB, false>(w, lut, sym, x, g, lo_g, 0, 0);
+        w.template flush<S>(oblo, 0, wo, we);
       }
+      break;
     }
-    while (next_state < 3) next_task_step();
+    const int32_t lo_group_end = lo_g;
+    if constexpr (!FUSED) {
+      while (next_state < 3) next_task_step();
+    }
     if (end_cursor != kNoEndCheck) {
       // the task reached its codec's first symbol: the outputs emitted before
       // group 0 (Eq. 3 with f(s_0) 2^(32-n) <= L, i.e. n = 16 and f = 1) are read last
@@ -630,14 +749,22 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     bool bad_end = false;
     const bool under = cursor < -1;
     if (end_cursor != kNoEndCheck) {
-      const bool lane_ok = (init_group < lo_group) || x == kL;
+      const bool lane_ok = (init_group < lo_group_end) || x == kL;
       bad_end = (cursor != (int)end_cursor) || !__all_sync(kFull, lane_ok);
     }
     if (lane == 0 && (bad_end || under)) {
       atomicOr(&p.status->flags, (under ? 1u : 0u) | (bad_end ? 2u : 0u));
       atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
     }
-    t = t_next;
+    if constexpr (FUSED) {
+      t = steal();  // the chain ended: next entry point (synchronous; entries are rare)
+      if (t < n_tasks) {
+        load_head(t);
+        load_windows();
+      }
+    } else {
+      t = t_next;
+    }
     buf ^= 1;
   }
   cp_wait<0>();
@@ -741,6 +868,12 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.ad_K = d->ad_K;
   prm.ad_E = d->ad_E;
   prm.nbits = pl.prob_bits;
+  prm.claims = reinterpret_cast<uint32_t *>(ws + d->claims_off);
+  if (++d->epoch == 0) {  // 2^32 decodes of one upload: clear the claims and restart the epochs
+    if (cudaMemsetAsync(ws + d->claims_off, 0, d->claims_bytes, s) != cudaSuccess) return RECOIL_E_CUDA;
+    d->epoch = 1;
+  }
+  prm.epoch = d->epoch;
   const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
   fn<<<grid, dev::kThreads, dyn_smem(*d), s>>>(prm);
@@ -773,6 +906,9 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   if (d->rec_len && cudaMemcpyAsync(ws + d->rec_off, d->c->bytes + d->rec_src, d->rec_len, cudaMemcpyHostToDevice,
                                     s) != cudaSuccess)
     return RECOIL_E_CUDA;
+  if (d->claims_bytes && cudaMemsetAsync(ws + d->claims_off, 0, d->claims_bytes, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  d->epoch = 0;
   uint64_t have = d->c->B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c->B - p.word_lo) : 0;
   if (have && cudaMemcpyAsync(d_words, d->c->words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
                   cudaSuccess)

@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.." && mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 timeout 1500 python -m pytest tests/ -x -q -m gpu --durations=15 > gpurun_out/pytest_full_$TAG.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_c2_$TAG.json 2> gpurun_out/bench_c2_$TAG.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_mp2_$TAG.json 2> gpurun_out/bench_mp2_$TAG.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu --no-adaptive > gpurun_out/bench_mp2_$TAG.json 2> gpurun_out/bench_mp2_$TAG.err
 timeout 600 python bench.py --config config1 --steps 50 --no-extra > gpurun_out/bench_c1_$TAG.json 2> gpurun_out/bench_c1_$TAG.err
 for lam in 10 50 200; do timeout 600 python bench.py --config config3 --lam $lam --steps 20 --no-extra --no-cpu > gpurun_out/bench_c3_l${lam}_$TAG.json 2> gpurun_out/bench_c3_l${lam}_$TAG.err; done
 for tgt in 2048 256 16; do timeout 600 python bench.py --config config4 --combine-to $tgt --steps 10 --no-extra --no-cpu > gpurun_out/bench_c4_${tgt}_$TAG.json 2> gpurun_out/bench_c4_${tgt}_$TAG.err; done
