@@ -154,6 +154,21 @@ def cpu_oracle_decode_rate(container: np.ndarray, sample_tasks: int | None, reps
     return nsym / best / 1e9, nsym, best, f"oracle or_recoil_decode_tasks on {len(tasks)} of {M} tasks ({nsym} symbols)"
 
 
+def smem_roofline(prof: dict, avg_ms: float, clocks, sms: int):
+    """The kernel's binding resource: shared-memory wavefronts (LUT gather, ring word, staging store;
+    DESIGN.md §7) per launch from the ncu capture of the same command (profiles/ncu_traffic.json), over
+    the event-timed launch, against 1 wavefront per SM-cycle at the clock sampled during the run."""
+    wf = prof.get("smem_wavefronts_per_launch")
+    if not wf or avg_ms <= 0:
+        return None
+    mhz = (clocks.report() or {}).get("sm_mhz") or 1965.0
+    peak = sms * mhz * 1e6
+    achieved = wf / (avg_ms / 1e3)
+    return {"bound": "smem", "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2),
+            "unit": "G wavefronts/s", "frac": round(achieved / peak, 4), "wavefronts_per_launch": int(wf),
+            "source": prof.get("source")}
+
+
 def peak_hbm() -> float:
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") or 6650.0)
@@ -415,6 +430,19 @@ def main():
             "recoil_combined_to_16": {"bytes": int(len(small)), "overhead_bytes": int(len(small) - len(c1))},
         }
         pdec.close()
+        if world == 1 and args.config == "config2" and not args.splits:
+            # Z26: BASELINE's "~20k-warp occupancy" split count (3 waves of resident warps)
+            M20 = 3 * warps * sms
+            c20 = R.recoil_encode(sym, f, 11, M20)
+            d20 = R.GpuDecoder(c20, local, stream=stream)
+            d20.upload()
+            d20.decode()
+            ok20 = d20.status()[0] == 0 and bool((d20.output().cpu().numpy() == sym).all())
+            t20 = timed_decode(d20, args.steps, args.warmup)
+            extra["config2_20k"] = {"value": round(N_total * args.steps / (sum(t20) / 1e3) / 1e9, 2), "unit": "GB/s",
+                                    "splits": R.recoil_inspect(c20)["n_splits"], "bit_exact": ok20,
+                                    "ms_per_step": round(float(np.mean(t20)), 4)}
+            d20.close()
         if world == 1 and not args.no_adaptive:
             extra["adaptive_latent"] = adaptive_extra(args, local, stream, timed_decode, peak_hbm())
     cpu = None
@@ -474,6 +502,7 @@ def main():
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "note": "achieved = (decoded bytes written + compressed words read + task table) / "
                                  "event-timed decode; peak = MEASURED_PEAKS.json hbm_gbs (burst)"},
+            "roofline_smem": smem_roofline(prof, my_avg_ms, clocks, sms),
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": int(plan["upload_bytes"]), "d2h_bytes_per_step": int(n_rank),

@@ -156,7 +156,6 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (!d.finals.empty()) std::memcpy(stg + d.finals_off, d.finals.data(), 4 * d.finals.size());
       if (!d.tasks.empty()) std::memcpy(stg + d.tasks_off, d.tasks.data(), sizeof(TaskRec) * d.tasks.size());
       if (!d.heads.empty()) std::memcpy(stg + d.tasks_off, d.heads.data(), sizeof(TaskHead) * d.heads.size());
-      if (d.claims_bytes) std::memset(stg + d.claims_off, 0, d.claims_bytes);  // fresh decoder: epoch 1
       const uint64_t staged_bytes = d.fused ? d.rec_off : pn.workspace_bytes;  // raw records: from the container
       if (cudaMemcpyAsync(ws, stg, staged_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaEventRecord(pl->staged[s], st) != cudaSuccess)

@@ -189,9 +189,7 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   d->lut_off = 16;
   d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
-  d->claims_off = align16(d->tasks_off + sizeof(TaskHead) * d->heads.size());
-  d->claims_bytes = 4 * d->heads.size();
-  d->rec_off = align16(d->claims_off + d->claims_bytes);
+  d->rec_off = align16(d->tasks_off + sizeof(TaskHead) * d->heads.size());
   p.workspace_bytes = align16(d->rec_off + d->rec_len + 256);  // + over-read pad of the record windows
   p.upload_bytes = (p.workspace_bytes - 16) + 2 * std::min<uint64_t>(p.word_count, c.B > word_lo ? c.B - word_lo : 0);
   return RECOIL_OK;

@@ -109,8 +109,6 @@ struct Decoder {
   std::vector<TaskHead> heads;
   uint64_t rec_src = 0, rec_len = 0;  // container byte span of the records the plan needs
   uint64_t lut_off = 0, finals_off = 0, tasks_off = 0, rec_off = 0;  // workspace byte offsets
-  uint64_t claims_off = 0, claims_bytes = 0;  // fused: per-task claim words (zeroed at upload)
-  uint32_t epoch = 0;                          // fused: claim epoch of the last decode
   uint32_t n_tasks = 0;
   int single_symbol = -1;          // >= 0: the model has one symbol (f = 2^n): decode = fill
   uint32_t ad_K = 0, ad_E = 0;     // adaptive: models, table entries (lut = coarse | entries | offsets)

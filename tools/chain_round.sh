@@ -8,4 +8,4 @@ for args in "--config config2 --waves 1" "--config config2 --waves 2" "--config 
   r=$(timeout 600 python bench.py $args --steps 20 --no-cpu --no-extra 2>/dev/null | tail -1)
   echo "$args $(python -c "import json; d=json.loads('''$r'''); print(d['value'], d['bit_exact'], d['ms_per_step'], d['config']['splits'])" 2>&1 | tail -1)"
 done | tee gpurun_out/chain_$TAG.txt
-tail -3 gpurun_out/smoke_$TAG.log gpurun_out/pytest_$TAG.log
+tail -n 3 gpurun_out/smoke_$TAG.log gpurun_out/pytest_$TAG.log

@@ -1,3 +1,5 @@
+// EXPERIMENT (not built): the decode kernel with chained tasks + work stealing (a3).
+// Kept for reference; measured 3-4 % slower than the atomic-counter scheduler at the bench configs.
 // decode.cu -- the Recoil decode kernel for sm_100a and its C-ABI entry points
 // (recoil_decoder_upload / recoil_decode / recoil_decoder_status /
 // recoil_decode_occupancy / recoil_decoder_launches).
@@ -29,6 +31,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cstring>
 
 #include "../recoil_internal.h"
@@ -79,6 +85,10 @@ struct Params {
   // aligned), model count, table entries, n
   const uint8_t *mid;
   uint32_t ad_K, ad_E, nbits;
+  // fused plans: per-task claim words (atomicMax with the decode's epoch)
+  uint32_t *claims;
+  uint32_t epoch;
+  uint32_t sched;  // experiments (env RECOIL_SCHED): bit 0 no continuation, bit 1 no stealing
 };
 
 // Static shared memory per block (about 33 KB for n = 11): the word rings need
@@ -99,6 +109,10 @@ struct __align__(16) Smem {
   // NB = 0 (adaptive): the model ids of each warp's current output block (8 x 512 B).
   uint32_t lut[NB == 0 ? 1024 : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512];
   uint16_t ring[kWarpsPerBlock][kRingWords];   // 8 x 2 KB word windows
+  // per-warp stash of the task state that is only needed between tasks (keeps
+  // it out of registers during the steady-state loop): lo, end cursor, task id,
+  // task index, all-initialised flag, the lanes' init groups, the chain's write bound
+  uint32_t scratch[kWarpsPerBlock][44];
 };
 constexpr int kOrLutMaxBits = 11;  // LUT base alignment trick up to 8 KB
 
@@ -122,6 +136,9 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -328,8 +345,12 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
   return x;
 }
 
-template <int NB, bool FUSED>
+template <int NB, bool FUSED, bool CHAIN>
 __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kernel(const Params p) {
+  // CHAIN (fused plans with more than two tasks per resident warp): chained
+  // tasks with work stealing; otherwise the atomic task counter (its steady
+  // state keeps more registers, measured 3-4 % faster at one or two tasks per warp)
+  constexpr bool kChain = FUSED && CHAIN;
   __shared__ Smem<NB> sm;
   extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
 
@@ -416,14 +437,52 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       pf_pr = (flags & kHeadFirst) ? 0u : ld_win(p.recs + ((rec_prev + 64) & ~3u), lane);
     }
   };
-  uint32_t t = blockIdx.x * kWarpsPerBlock + warp;
+  // Fused plans (Recoil): chained tasks with work stealing.  A warp that
+  // finishes task t is synchronised and simply keeps decoding into task t-1
+  // (no Synchronization Phase: the Cross-Boundary Phase of P:314 extended over
+  // whole tasks) if it can claim t-1; claims are atomicMax of the decode's
+  // epoch into a per-task word.  Warp gw starts at the top of its segment of
+  // seg = ceil(tasks / warps) tasks; a warp whose chain runs into a claimed task
+  // steals an entry point: candidates are the segment midpoints, then the
+  // quarter points, ... (level-major over all segments), so a fast warp
+  // splits the largest unclaimed runs of slow warps.  Every task is decoded
+  // exactly once; a Synchronization Phase runs only at entry points.
+  const uint32_t n_tasks = p.n_tasks;
+  const uint32_t Wg = gridDim.x * kWarpsPerBlock;
+  const uint32_t gw = blockIdx.x * kWarpsPerBlock + warp;
+  const uint32_t seg = kChain ? max(1u, (n_tasks + Wg - 1) / Wg) : 1u;
+  uint32_t levels = 0;
+  while ((seg >> (levels + 1)) > 0) ++levels;
+  auto claim = [&](uint32_t t) -> bool {  // warp-uniform
+    uint32_t old = 0;
+    if (lane == 0) old = atomicMax(&p.claims[t], p.epoch);
+    return __shfl_sync(kFull, old, 0) < p.epoch;
+  };
+  auto steal = [&]() -> uint32_t {  // next entry point, or n_tasks
+    for (;;) {
+      uint32_t k = 0;
+      if (lane == 0) k = atomicAdd(&p.status->next_task, 1u);
+      k = __shfl_sync(kFull, k, 0);
+      if (k >= Wg * levels || (p.sched & 2u)) return n_tasks;
+      const uint32_t g = k % Wg, o = seg >> (k / Wg + 1);
+      const uint32_t t = g * seg + o - 1;
+      if (t < n_tasks && claim(t)) return t;
+    }
+  };
+  uint32_t t;
+  if constexpr (kChain) {
+    t = gw * seg < n_tasks ? min(n_tasks, (gw + 1) * seg) - 1 : n_tasks;
+    if (t < n_tasks && !claim(t)) t = steal();
+  } else {
+    t = gw;
+  }
   int buf = 0;
-  if (t < p.n_tasks) {
+  if (t < n_tasks) {
     issue_task(t, 0);
     load_head(t);
     load_windows();
   }
-  while (t < p.n_tasks) {
+  while (t < n_tasks) {
     cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
     int32_t start_group, init_group, cursor0;
@@ -514,6 +573,35 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       }
     };
 
+    // fused: continuation into task t_cur - 1.  0 = not asked, 1 = claim atomic
+    // in flight, 2 = head in flight, 3 = record window in flight
+    const uint32_t scr = smem_addr(&sm.scratch[warp][0]);
+    uint32_t c_old = 0;
+    int cstate = 0;
+    bool cgot = false;
+    auto chain_step = [&]() {
+      if (cstate == 0) {
+        const uint32_t t_cur = lds_u32(scr + 20);
+        if (lane == 0 && t_cur > 0 && !(p.sched & 1u)) c_old = atomicMax(&p.claims[t_cur - 1], p.epoch);
+        else c_old = p.epoch;
+        cstate = 1;
+      } else if (cstate == 1) {
+        const uint32_t t_cur = lds_u32(scr + 20);
+        cgot = t_cur > 0 && __shfl_sync(kFull, c_old, 0) < p.epoch;
+        if (cgot) load_head(t_cur - 1);
+        cstate = 2;
+      } else if (cstate == 2) {
+        if (cgot) {
+          const uint32_t rec_prev = __shfl_sync(kFull, hw, 3), flags = __shfl_sync(kFull, hw, 5);
+          pf_pr = (flags & kHeadFirst) ? 0u : ld_win(p.recs + ((rec_prev + 64) & ~3u), lane);
+        }
+        cstate = 3;
+      }
+    };
+    auto tail_step = [&]() {
+      if constexpr (kChain) chain_step(); else next_task_step();
+    };
+
     // a7: word window -- chunks c, c-1, c-2 resident, c-3 in flight
     w.cursor2 = 2 * cursor0;
     w.cchunk = cursor0 >> 8;
@@ -540,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     // memory (16 B per lane); the next lower block's ids are loaded into
     // registers meanwhile (one block of look-ahead)
     uint4 midv = make_uint4(0, 0, 0, 0);
-    int mid_blk = -1;
+    int mid_blk = -1, staged_blk = -1;
     auto mid_load = [&](int blk) -> uint4 {
       const uint64_t N = ((uint64_t)p.N_hi << 32) | p.N_lo;
       const uint64_t i0 = (uint64_t)blk * kBlockBytes + 16 * lane;
@@ -557,6 +645,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
         __syncwarp();
         sts_v4(w.mid32 - lane + 16 * lane, v);
         __syncwarp();
+        staged_blk = blk;
         if (blk > 0) {
           midv = mid_load(blk - 1);
           mid_blk = blk - 1;
@@ -579,43 +668,128 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       g = ge - 1;
     }
     // a5 + a6: Decoding Phase and Cross-Boundary Phase (all lanes initialised)
-    if (g >= lo_group && (g & 15) != 15) {  // head: partial block
-      const int gb = g & ~15, ge = max(gb, lo_group);
-      if (g == start_group) stage_block(g >> 4);  // else staged by the sync phase
-      x = run_part<NB, false>(w, lut, sym, x, g, ge, 0, 0);
-      const int rel = (gb >> 4) - b_lo;
-      w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
-      g = ge - 1;
+    // all lanes initialised before the task's range ends (always, by Z9): only
+    // then may the warp continue into the next task without a sync phase
+    if constexpr (kChain) {
+      const bool all_init = min_init >= lo_group;
+      if (lane == 0) {
+        sts_u32(scr, (uint32_t)lo);
+        sts_u32(scr + 4, (uint32_t)(lo >> 32));
+        sts_u32(scr + 8, (uint32_t)end_cursor);
+        sts_u32(scr + 12, (uint32_t)((uint64_t)end_cursor >> 32));
+        sts_u32(scr + 16, task_id);
+        sts_u32(scr + 20, t);
+        sts_u32(scr + 24, all_init ? 1u : 0u);
+        sts_u32(scr + 160, (uint32_t)whi);  // the chain never writes above its entry task's bound
+        sts_u32(scr + 164, (uint32_t)(whi >> 32));
+      }
+      sts_u32(scr + 32 + 4 * lane, (uint32_t)init_group);
+      __syncwarp();
     }
-    if (g >= lo_group) {
-      // whole blocks above the block of lo_group; the next task id is requested
-      // three blocks before the end
-      int rel = (g >> 4) - b_lo;
-      const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      uint8_t *dst = out_blo + rel * kBlk;
-      int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
-      for (; rel >= full_lo + 3; --rel) {
-        stage_block(b_lo + rel);
-        x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
-        dst -= kBlk;
-        c -= kBlk;
+    int32_t lo_g = lo_group, blo = b_lo;
+    uint8_t *oblo = out_blo;
+    int wo = woff, we = wend;
+    for (;;) {
+      if (g >= lo_g && (g & 15) != 15) {  // partial top block: after the sync phase, or a continuation
+        const int gb = g & ~15, ge = max(gb, lo_g);       // that starts inside a block
+        if (staged_blk != (g >> 4)) stage_block(g >> 4);
+        x = run_part<NB, false>(w, lut, sym, x, g, ge, 0, 0);
+        const int rel = (gb >> 4) - blo;
+        w.template flush<S>(oblo + rel * kBlk, rel * kBlk, wo, we);
+        g = ge - 1;
       }
-      for (; rel >= full_lo; --rel) {
-        next_task_step();
-        stage_block(b_lo + rel);
-        x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
-        dst -= kBlk;
-        c -= kBlk;
+      if (g >= lo_g) {
+        // whole blocks above the block of lo_g; the continuation (fused) or the
+        // next task id is requested three blocks before the end
+        int rel = (g >> 4) - blo;
+        const int full_lo = ((lo_g & 15) == 0) ? 0 : 1;
+        uint8_t *dst = oblo + rel * kBlk;
+        int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
+        for (; rel >= full_lo + 3; --rel) {
+          stage_block(blo + rel);
+          x = run_block<NB>(w, lut, sym, x);
+          w.template flush_at<S>(dst, c, wo, we);
+          dst -= kBlk;
+          c -= kBlk;
+        }
+        for (; rel >= full_lo; --rel) {
+          tail_step();
+          stage_block(blo + rel);
+          x = run_block<NB>(w, lut, sym, x);
+          w.template flush_at<S>(dst, c, wo, we);
+          dst -= kBlk;
+          c -= kBlk;
+        }
+        g = (blo + full_lo) * 16 - 1;  // next group to decode
       }
-      if (full_lo) {  // tail: the partial block of lo_group
-        stage_block(b_lo);
-        x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
-        w.template flush<S>(out_blo, 0, woff, wend);
+      if constexpr (kChain) {
+        while (cstate < 3) chain_step();
+        if (cgot && lds_u32(scr + 24)) {
+          // continue into task t_cur - 1: its committed range ends where ours
+          // starts; its lower bound is the sync start of its own lower point
+          const uint32_t flags = __shfl_sync(kFull, hw, 5);
+          const uint32_t id_prev = __shfl_sync(kFull, hw, 6);
+          int64_t lo2 = 0;
+          bool bad2 = false;
+          if (!(flags & kHeadFirst)) {
+            const uint32_t rec_prev = __shfl_sync(kFull, hw, 3), maxg_prev = __shfl_sync(kFull, hw, 4);
+            uint32_t wdt;
+            const uint32_t d = series_elem(pf_pr, (rec_prev + 64) & 3u, lane, &wdt);
+            bad2 = d > maxg_prev;
+            int32_t idx = ((int32_t)maxg_prev - (int32_t)d) * 32 + lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
+            lo2 = idx;
+          }
+          const int64_t lo_cur = (int64_t)(((uint64_t)lds_u32(scr + 4) << 32) | lds_u32(scr));
+          bad2 |= lo2 >= lo_cur;
+          if (!__any_sync(kFull, bad2)) {
+            const int64_t ec = (flags & kHeadFirst) ? (int64_t)(int32_t)__shfl_sync(kFull, hw, 7) : kNoEndCheck;
+            __syncwarp();
+            if (lane == 0) {
+              sts_u32(scr, (uint32_t)lo2);
+              sts_u32(scr + 4, (uint32_t)((uint64_t)lo2 >> 32));
+              sts_u32(scr + 8, (uint32_t)ec);
+              sts_u32(scr + 12, (uint32_t)((uint64_t)ec >> 32));
+              sts_u32(scr + 16, id_prev);
+              sts_u32(scr + 20, lds_u32(scr + 20) - 1);
+            }
+            __syncwarp();
+            lo_g = (int32_t)(lo2 >> 5);
+            blo = lo_g >> 4;
+            oblo = p.out + ((uint64_t)blo * kBlockBytes - p.out_base) * S;
+            wo = (lo_g * (int)kLanes - blo * (int)kBlockBytes) * S;
+            {  // the entry task's write bound, relative to the new base block
+              const uint64_t whi_c = ((uint64_t)lds_u32(scr + 164) << 32) | lds_u32(scr + 160);
+              const int64_t rel_we = ((int64_t)whi_c - (int64_t)blo * kBlockBytes) * S;
+              we = rel_we < 0x7FFFFFFF ? (int)rel_we : 0x7FFFFFFF;
+            }
+            cstate = 0;
+            cgot = false;
+            continue;
+          }
+          if (lane == 0) {  // inconsistent metadata of the next task: flag it, end the chain
+            atomicOr(&p.status->flags, 4u);
+            atomicMax(&p.status->bad_task, 0xFFFFFFFFu - id_prev);
+          }
+        }
       }
+      if (g >= lo_g) {  // tail: the partial block of lo_g
+        stage_block(blo);
+        x = run_part<NB, false>(w, lut, sym, x, g, lo_g, 0, 0);
+        w.template flush<S>(oblo, 0, wo, we);
+      }
+      break;
     }
-    while (next_state < 3) next_task_step();
+    const int32_t lo_group_end = lo_g;
+    if constexpr (!kChain) {
+      while (next_state < 3) next_task_step();
+    }
+    if constexpr (kChain) {  // the chain's last task
+      end_cursor = (int64_t)(((uint64_t)lds_u32(scr + 12) << 32) | lds_u32(scr + 8));
+      task_id = lds_u32(scr + 16);
+      init_group = (int32_t)lds_u32(scr + 32 + 4 * lane);
+    }
     if (end_cursor != kNoEndCheck) {
       // the task reached its codec's first symbol: the outputs emitted before
       // group 0 (Eq. 3 with f(s_0) 2^(32-n) <= L, i.e. n = 16 and f = 1) are read last
@@ -630,58 +804,85 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     bool bad_end = false;
     const bool under = cursor < -1;
     if (end_cursor != kNoEndCheck) {
-      const bool lane_ok = (init_group < lo_group) || x == kL;
+      const bool lane_ok = (init_group < lo_group_end) || x == kL;
       bad_end = (cursor != (int)end_cursor) || !__all_sync(kFull, lane_ok);
     }
     if (lane == 0 && (bad_end || under)) {
       atomicOr(&p.status->flags, (under ? 1u : 0u) | (bad_end ? 2u : 0u));
       atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
     }
-    t = t_next;
+    if constexpr (kChain) {
+      t = steal();  // the chain ended: next entry point (synchronous; entries are rare)
+      if (t < n_tasks) {
+        load_head(t);
+        load_windows();
+      }
+    } else {
+      t = t_next;
+    }
     buf ^= 1;
   }
   cp_wait<0>();
 }
 
 using KernelFn = void (*)(const Params);
-static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false) {
-  if (adaptive) return fused ? recoil_decode_kernel<0, true> : nullptr;
+static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false, bool chain = false) {
+  if (adaptive) return !fused ? nullptr : chain ? recoil_decode_kernel<0, true, true> : recoil_decode_kernel<0, true, false>;
+  if (fused && chain) switch (nbits) {
+    case 1: return recoil_decode_kernel<1, true, true>;
+    case 2: return recoil_decode_kernel<2, true, true>;
+    case 3: return recoil_decode_kernel<3, true, true>;
+    case 4: return recoil_decode_kernel<4, true, true>;
+    case 5: return recoil_decode_kernel<5, true, true>;
+    case 6: return recoil_decode_kernel<6, true, true>;
+    case 7: return recoil_decode_kernel<7, true, true>;
+    case 8: return recoil_decode_kernel<8, true, true>;
+    case 9: return recoil_decode_kernel<9, true, true>;
+    case 10: return recoil_decode_kernel<10, true, true>;
+    case 11: return recoil_decode_kernel<11, true, true>;
+    case 12: return recoil_decode_kernel<12, true, true>;
+    case 13: return recoil_decode_kernel<13, true, true>;
+    case 14: return recoil_decode_kernel<14, true, true>;
+    case 15: return recoil_decode_kernel<15, true, true>;
+    case 16: return recoil_decode_kernel<16, true, true>;
+    default: return nullptr;
+  }
   if (fused) switch (nbits) {
-    case 1: return recoil_decode_kernel<1, true>;
-    case 2: return recoil_decode_kernel<2, true>;
-    case 3: return recoil_decode_kernel<3, true>;
-    case 4: return recoil_decode_kernel<4, true>;
-    case 5: return recoil_decode_kernel<5, true>;
-    case 6: return recoil_decode_kernel<6, true>;
-    case 7: return recoil_decode_kernel<7, true>;
-    case 8: return recoil_decode_kernel<8, true>;
-    case 9: return recoil_decode_kernel<9, true>;
-    case 10: return recoil_decode_kernel<10, true>;
-    case 11: return recoil_decode_kernel<11, true>;
-    case 12: return recoil_decode_kernel<12, true>;
-    case 13: return recoil_decode_kernel<13, true>;
-    case 14: return recoil_decode_kernel<14, true>;
-    case 15: return recoil_decode_kernel<15, true>;
-    case 16: return recoil_decode_kernel<16, true>;
+    case 1: return recoil_decode_kernel<1, true, false>;
+    case 2: return recoil_decode_kernel<2, true, false>;
+    case 3: return recoil_decode_kernel<3, true, false>;
+    case 4: return recoil_decode_kernel<4, true, false>;
+    case 5: return recoil_decode_kernel<5, true, false>;
+    case 6: return recoil_decode_kernel<6, true, false>;
+    case 7: return recoil_decode_kernel<7, true, false>;
+    case 8: return recoil_decode_kernel<8, true, false>;
+    case 9: return recoil_decode_kernel<9, true, false>;
+    case 10: return recoil_decode_kernel<10, true, false>;
+    case 11: return recoil_decode_kernel<11, true, false>;
+    case 12: return recoil_decode_kernel<12, true, false>;
+    case 13: return recoil_decode_kernel<13, true, false>;
+    case 14: return recoil_decode_kernel<14, true, false>;
+    case 15: return recoil_decode_kernel<15, true, false>;
+    case 16: return recoil_decode_kernel<16, true, false>;
     default: return nullptr;
   }
   switch (nbits) {
-    case 1: return recoil_decode_kernel<1, false>;
-    case 2: return recoil_decode_kernel<2, false>;
-    case 3: return recoil_decode_kernel<3, false>;
-    case 4: return recoil_decode_kernel<4, false>;
-    case 5: return recoil_decode_kernel<5, false>;
-    case 6: return recoil_decode_kernel<6, false>;
-    case 7: return recoil_decode_kernel<7, false>;
-    case 8: return recoil_decode_kernel<8, false>;
-    case 9: return recoil_decode_kernel<9, false>;
-    case 10: return recoil_decode_kernel<10, false>;
-    case 11: return recoil_decode_kernel<11, false>;
-    case 12: return recoil_decode_kernel<12, false>;
-    case 13: return recoil_decode_kernel<13, false>;
-    case 14: return recoil_decode_kernel<14, false>;
-    case 15: return recoil_decode_kernel<15, false>;
-    case 16: return recoil_decode_kernel<16, false>;
+    case 1: return recoil_decode_kernel<1, false, false>;
+    case 2: return recoil_decode_kernel<2, false, false>;
+    case 3: return recoil_decode_kernel<3, false, false>;
+    case 4: return recoil_decode_kernel<4, false, false>;
+    case 5: return recoil_decode_kernel<5, false, false>;
+    case 6: return recoil_decode_kernel<6, false, false>;
+    case 7: return recoil_decode_kernel<7, false, false>;
+    case 8: return recoil_decode_kernel<8, false, false>;
+    case 9: return recoil_decode_kernel<9, false, false>;
+    case 10: return recoil_decode_kernel<10, false, false>;
+    case 11: return recoil_decode_kernel<11, false, false>;
+    case 12: return recoil_decode_kernel<12, false, false>;
+    case 13: return recoil_decode_kernel<13, false, false>;
+    case 14: return recoil_decode_kernel<14, false, false>;
+    case 15: return recoil_decode_kernel<15, false, false>;
+    case 16: return recoil_decode_kernel<16, false, false>;
     default: return nullptr;
   }
 }
@@ -706,13 +907,26 @@ static int occupancy(dev::KernelFn fn, size_t dyn, int *blocks_per_sm) {
   return RECOIL_OK;
 }
 
+// cudaFuncSetAttribute for every kernel variant actually launched (once per process per size)
+static int occupancy_once(dev::KernelFn fn, size_t dyn) {
+  static std::mutex mu;
+  static std::vector<std::pair<dev::KernelFn, size_t>> done;  // (kernel, largest dynamic smem configured)
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto &e : done)
+    if (e.first == fn && e.second >= dyn) return RECOIL_OK;
+  int bps = 0;
+  int rc = occupancy(fn, dyn, &bps);
+  if (rc == RECOIL_OK) done.emplace_back(fn, dyn);
+  return rc;
+}
+
 static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *d_mid, uint8_t *d_out,
                   cudaStream_t s) {
   const recoil_plan &pl = d->plan;
   const bool adaptive = d->c->adaptive;
-  dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive);
   if (d->blocks_per_sm == 0) {
-    int rc = occupancy(fn, dyn_smem(*d), &d->blocks_per_sm);
+    // occupancy of the chained kernel (same resources as the counter-scheduled one)
+    int rc = occupancy(dev::kernel_for(pl.prob_bits, d->fused, adaptive, true), dyn_smem(*d), &d->blocks_per_sm);
     if (rc) return rc;
     int dev_id = 0;
     if (cudaGetDevice(&dev_id) != cudaSuccess ||
@@ -720,6 +934,10 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
       return RECOIL_E_CUDA;
     if (d->blocks_per_sm < 1) return RECOIL_E_UNSUPPORTED;  // tables do not fit in shared memory
   }
+  // more than two tasks per resident warp: chained tasks + work stealing (fused plans)
+  const bool chain = d->fused && (uint64_t)pl.n_tasks > 2ull * d->blocks_per_sm * d->sm_count * dev::kWarpsPerBlock;
+  dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive, chain);
+  if (!fn || occupancy_once(fn, dyn_smem(*d)) != RECOIL_OK) return RECOIL_E_CUDA;
   dev::Params prm;
   prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
   prm.finals = reinterpret_cast<const uint32_t *>(ws + d->finals_off);
@@ -741,6 +959,17 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.ad_K = d->ad_K;
   prm.ad_E = d->ad_E;
   prm.nbits = pl.prob_bits;
+  prm.claims = reinterpret_cast<uint32_t *>(ws + d->claims_off);
+  if (++d->epoch == 0) {  // 2^32 decodes of one upload: clear the claims and restart the epochs
+    if (cudaMemsetAsync(ws + d->claims_off, 0, d->claims_bytes, s) != cudaSuccess) return RECOIL_E_CUDA;
+    d->epoch = 1;
+  }
+  prm.epoch = d->epoch;
+  static const uint32_t sched_env = [] {
+    const char *e = getenv("RECOIL_SCHED");
+    return e ? (uint32_t)atoi(e) : 0u;
+  }();
+  prm.sched = sched_env;
   const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
   fn<<<grid, dev::kThreads, dyn_smem(*d), s>>>(prm);
@@ -773,6 +1002,9 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   if (d->rec_len && cudaMemcpyAsync(ws + d->rec_off, d->c->bytes + d->rec_src, d->rec_len, cudaMemcpyHostToDevice,
                                     s) != cudaSuccess)
     return RECOIL_E_CUDA;
+  if (d->claims_bytes && cudaMemsetAsync(ws + d->claims_off, 0, d->claims_bytes, s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  d->epoch = 0;
   uint64_t have = d->c->B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c->B - p.word_lo) : 0;
   if (have && cudaMemcpyAsync(d_words, d->c->words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=
                   cudaSuccess)
