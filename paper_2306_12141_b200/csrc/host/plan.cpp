@@ -58,9 +58,14 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
   const uint32_t E = off[K];
   if (E > 65535) return RECOIL_E_UNSUPPORTED;
   const uint32_t Epad = (E + 3) & ~3u;
-  std::vector<uint32_t> w((size_t)K * 64 + Epad + K, 0);
-  uint32_t *coarse = w.data(), *ent = w.data() + (size_t)K * 64, *delta = ent + Epad;
-  const uint32_t shift = n > 6 ? n - 6 : 0, nb = 1u << (n - shift);
+  // coarse buckets per model: 2^cbits, the largest (<= 64) whose tables fit
+  // kAdaptiveTableBudget (fewer buckets = longer binary searches)
+  uint32_t cbits = 6;
+  while (cbits > 3 && 4ull * (((uint64_t)K << cbits) + Epad + K) > kAdaptiveTableBudget) --cbits;
+  const uint32_t nbk = 1u << cbits;
+  std::vector<uint32_t> w((size_t)K * nbk + Epad + K, 0);
+  uint32_t *coarse = w.data(), *ent = w.data() + (size_t)K * nbk, *delta = ent + Epad;
+  const uint32_t shift = n > cbits ? n - cbits : 0, nb = 1u << (n - shift);
   std::vector<uint32_t> F;
   for (uint32_t k = 0; k < K; ++k) {
     F.assign(keep[k], 0);
@@ -77,16 +82,16 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
       uint32_t j = (uint32_t)(std::upper_bound(F.begin(), F.end(), slot) - F.begin());
       return off[k] + (j ? j - 1 : 0);
     };
-    for (uint32_t b = 0; b < 64; ++b) {
+    for (uint32_t b = 0; b < nbk; ++b) {
       const uint32_t bb = std::min(b, nb - 1);
       const uint32_t s0 = bb << shift, s1 = ((bb + 1) << shift) - 1;
-      coarse[k * 64 + b] = entry_of(s0) | (entry_of(s1) << 16);
+      coarse[k * nbk + b] = entry_of(s0) | (entry_of(s1) << 16);
     }
   }
   blob->resize(4 * w.size());
   std::memcpy(blob->data(), w.data(), blob->size());
   *Kout = K;
-  *Eout = E;
+  *Eout = E | (cbits << 24);  // E < 2^16; the coarse bucket bits ride in the top byte
   return RECOIL_OK;
 }
 

@@ -177,7 +177,7 @@ struct Warp {
   // adaptive (NB = 0): this lane's model-id slot of the staged block, the
   // model tables (coarse bucket -> entry range, entries F | (f-1) << 16,
   // per-model value offset), n, the coarse shift and the largest model id
-  uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax;
+  uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax, cbits;
   uint32_t gt;       // lanes above this one
   int lane;
   int cursor2;       // 2 x (slice-relative index of the next word to read)
@@ -226,7 +226,7 @@ struct Warp {
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
       const uint32_t slot = x & ((1u << nb) - 1);
-      const uint32_t cb = lds_u32(coarse32 + (((km << 6) + (slot >> cshift)) << 2));
+      const uint32_t cb = lds_u32(coarse32 + (((km << cbits) + (slot >> cshift)) << 2));
       uint32_t lo = cb & 0xFFFFu, hi = cb >> 16;
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
@@ -336,7 +336,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   constexpr int S = sym_bytes<NB>();
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
-    const uint32_t words = p.ad_K * 64 + ((p.ad_E + 3) & ~3u) + p.ad_K;
+    const uint32_t ent_n = p.ad_E & 0xFFFFFFu, cbits = p.ad_E >> 24;
+    const uint32_t words = (p.ad_K << cbits) + ((ent_n + 3) & ~3u) + p.ad_K;
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
@@ -367,11 +368,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   w.lut32 = smem_addr(sm.lut);
   if constexpr (NB == 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
+    w.cbits = p.ad_E >> 24;
     w.coarse32 = smem_addr(sym_dyn);
-    w.ent32 = w.coarse32 + 256 * p.ad_K;
-    w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
+    w.ent32 = w.coarse32 + 4 * (p.ad_K << w.cbits);
+    w.delta32 = w.ent32 + 4 * (((p.ad_E & 0xFFFFFFu) + 3) & ~3u);
     w.nb = p.nbits;
-    w.cshift = p.nbits > 6 ? p.nbits - 6 : 0;
+    w.cshift = p.nbits > w.cbits ? p.nbits - w.cbits : 0;
     w.kmax = p.ad_K - 1;
   }
   if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
