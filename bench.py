@@ -259,6 +259,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
     ap.add_argument("--no-adaptive", action="store_true", help="skip the adaptive-codec extra")
+    ap.add_argument("--gather", action="store_true",
+                    help="N > 1: time the optional NCCL gather of the ranks' spans to rank 0 (outside the decode)")
     ap.add_argument("--waves", type=int, default=0,
                     help="splits per GPU = waves x resident warps; 0 = per-config default (config2: 1, one split "
                          "per resident warp, the decoder-adaptive choice of P:84; configs 3/5: 2, measured best for "
@@ -406,6 +408,27 @@ def main():
     ok = ok and bool((out_host.numpy()[plan["out_lo"]:plan["out_hi"]] == sym[plan["out_lo"]:plan["out_hi"]]).all())
 
     extra = {}
+    if pg and args.gather:
+        # row a10: optional final gather of every rank's committed span to rank 0 over NCCL
+        # (its own process group; the timed decode above has no data-path exchange)
+        nccl = pg.new_group(backend="nccl")
+        spans = R.shard_spans(cont, world)
+        full = torch.empty(N_total, dtype=torch.uint8, device=dev) if rank == 0 else None
+        gts = []
+        for i in range(4):
+            torch.cuda.synchronize(dev)
+            pg.barrier()
+            t0 = time.perf_counter()
+            R.gather_spans(dec.output(), spans, root=0, out=full, group=nccl)
+            torch.cuda.synchronize(dev)
+            gts.append(time.perf_counter() - t0)
+        gt = float(np.median(gts[1:]))
+        t = torch.tensor([gt], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        gok = bool((full.cpu().numpy() == sym).all()) if rank == 0 else True
+        extra["gather"] = {"ms": round(float(t.item()) * 1e3, 3), "bytes": int(N_total - n_rank) if rank == 0 else 0,
+                           "GB/s_into_root": round((N_total - n_rank) / float(t.item()) / 1e9, 2), "bit_exact": gok,
+                           "backend": "nccl", "note": "rank spans -> rank 0, batched point-to-point; not in value"}
     if rank == 0 and not args.no_extra:
         # the paper's comparison: conventional partitioned decoder at the same count
         pc = R.recoil_partitioned_encode(sym, f, 11, M)

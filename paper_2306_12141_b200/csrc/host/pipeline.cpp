@@ -163,6 +163,9 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (d.rec_len && cudaMemcpyAsync(ws + d.rec_off, c->bytes + d.rec_src, d.rec_len, cudaMemcpyHostToDevice,
                                        st) != cudaSuccess)
         return RECOIL_E_CUDA;
+      if (d.fused && cudaMemsetAsync(ws + d.rec_off + d.rec_len, 0, pn.workspace_bytes - d.rec_off - d.rec_len, st) !=
+                         cudaSuccess)  // pad under the record windows
+        return RECOIL_E_CUDA;
       const uint64_t have = c->B > pn.word_lo ? std::min<uint64_t>(pn.word_count, c->B - pn.word_lo) : 0;
       if (have && cudaMemcpyAsync(words, c->words + 2 * pn.word_lo, 2 * have, cudaMemcpyHostToDevice, st) !=
                       cudaSuccess)

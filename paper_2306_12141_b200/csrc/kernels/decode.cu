@@ -196,6 +196,7 @@ struct Warp {
   __device__ __forceinline__ void window_check() {
     const int c = cursor2 >> 9;
     if (c != cchunk) {
+      __syncwarp();  // all lanes' reads of the slot being refilled (chunk c+1's) are done
       do {
         --cchunk;
         issue_chunk(cchunk - 3);
@@ -774,6 +775,10 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
     return RECOIL_E_CUDA;
   if (d->rec_len && cudaMemcpyAsync(ws + d->rec_off, d->c->bytes + d->rec_src, d->rec_len, cudaMemcpyHostToDevice,
                                     s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  // the 128-B record windows may reach past the last record: zero that pad
+  if (d->fused && cudaMemsetAsync(ws + d->rec_off + d->rec_len, 0, p.workspace_bytes - d->rec_off - d->rec_len, s) !=
+                      cudaSuccess)
     return RECOIL_E_CUDA;
   uint64_t have = d->c->B > p.word_lo ? std::min<uint64_t>(p.word_count, d->c->B - p.word_lo) : 0;
   if (have && cudaMemcpyAsync(d_words, d->c->words + 2 * p.word_lo, 2 * have, cudaMemcpyHostToDevice, s) !=

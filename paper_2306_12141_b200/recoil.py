@@ -452,3 +452,44 @@ def decode_gpu(container, device: int = 0):
     out = dec.output().clone()
     dec.close()
     return out
+
+
+# --- multi-GPU (§8(e), row a10): optional gather of the shards' spans ----------------------
+
+def shard_spans(container, world: int) -> list[tuple[int, int, int, int]]:
+    """(task_begin, task_end, out_lo, out_hi) of every rank's shard of `container`
+    (recoil_shard_plan + the decoder plans; host only, identical on every rank)."""
+    c = _u8(container)
+    bounds = recoil_shard_plan(c, world)
+    spans = []
+    for a, b in zip(bounds, bounds[1:]):
+        h = recoil_decoder_create(c, a, b)
+        p = recoil_decoder_plan(h)
+        recoil_decoder_destroy(h)
+        spans.append((a, b, p["out_lo"], p["out_hi"]))
+    return spans
+
+
+def gather_spans(span, spans, root: int = 0, out=None, group=None):
+    """Optional final gather (north_star: "NCCL is used only for an optional final
+    gather"): every rank sends its committed span (a tensor of out_hi - out_lo
+    symbols, on its GPU for NCCL) to `root`, which receives them into `out` (a
+    tensor of N symbols, allocated if None) with one batch of point-to-point
+    operations.  The decode itself has no data-path exchange; this is
+    outside the timed decode.  Returns `out` on root, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    if rank != root:
+        dist.batch_isend_irecv([dist.P2POp(dist.isend, span.contiguous(), root, group)])[0].wait()
+        return None
+    n_total = spans[-1][3]
+    if out is None:
+        out = torch.empty(n_total, dtype=span.dtype, device=span.device)
+    lo, hi = spans[root][2], spans[root][3]
+    out[lo:hi].copy_(span)
+    ops = [dist.P2POp(dist.irecv, out[spans[r][2]:spans[r][3]], r, group) for r in range(world) if r != root]
+    for w in dist.batch_isend_irecv(ops) if ops else []:
+        w.wait()
+    return out

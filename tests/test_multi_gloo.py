@@ -91,3 +91,44 @@ def test_two_rank_shards_gloo(kind, part, M):
     tiles, exact, sizes = q.get(timeout=10)
     assert tiles and exact, sizes
     assert min(sizes) > 0.3 * max(sizes)
+
+
+def _gather_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import synth
+    from paper_2306_12141_b200 import recoil as R
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sym = synth.workload("text", 300_000, seed=5)
+        f = R.recoil_build_model(synth.histogram(sym), 11)
+        c = R.recoil_encode(sym, f, 11, 200)
+        spans = R.shard_spans(c, world)
+        _, _, lo, hi = spans[rank]
+        # this rank's decoded span (CPU decode of the whole stream stands in for the GPU shard)
+        mine = torch.from_numpy(R.recoil_decode_cpu(c)[lo:hi].copy())
+        full = R.gather_spans(mine, spans, root=0)
+        if rank == 0:
+            q.put((bool((full.numpy() == sym).all()), [s[3] - s[2] for s in spans]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_optional_gather_of_shard_spans(world):
+    """Row a10: the optional final gather reassembles the stream on the root from the
+    ranks' committed spans (point-to-point batch; gloo here, NCCL on GPUs)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    ok, sizes = q.get(timeout=5)
+    assert ok and len(sizes) == world and min(sizes) > 0

@@ -19,6 +19,18 @@ for kind, N, n, M, part in (("exp", 300000, 11, 64, False), ("text", 200000, 12,
         out = dec.output().cpu().numpy()
         ok &= rc == 0 and bool((out == sym[p["out_lo"]:p["out_hi"]]).all())
         dec.close()
+# adaptive codec (index-keyed models, 16-bit symbols)
+lsym, mid, h = synth.latent_workload(150000, 4)
+fm = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
+ca = R.recoil_encode_adaptive(lsym, mid, {"base": h["base"], "len": h["len"], "f": fm}, 16, 40)
+for a, b in ((0, 1 << 64 - 1), tuple(R.recoil_shard_plan(ca, 2)[:2])):
+    dec = R.GpuDecoder(ca, 0, a, b)
+    dec.set_model_ids(mid)
+    dec.upload(); dec.decode(); rc, bad = dec.status()
+    p = dec.plan
+    out = dec.output().cpu().numpy().view(np.uint16)
+    ok &= rc == 0 and bool((out == lsym[p["out_lo"]:p["out_hi"]]).all())
+    dec.close()
 print("decodes ok" if ok else "DECODE MISMATCH")
 PY
 for tool in memcheck racecheck synccheck initcheck; do
