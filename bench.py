@@ -268,6 +268,7 @@ def main():
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
     ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
     ap.add_argument("--chunks", type=int, default=8, help="e2e pipeline chunks per GPU")
+    ap.add_argument("--streams", type=int, default=3, help="e2e pipeline streams per GPU")
     ap.add_argument("--lam", type=float, default=0.0, help="config3/4: override lambda")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -382,7 +383,7 @@ def main():
     # the kernels, D2H of the symbols into pinned memory, status read; chunks on 3
     # streams so copies overlap kernels and each other.
     out_host = torch.empty(max(N_total, 16), dtype=torch.uint8, pin_memory=True)
-    pipe = R.HostPipeline(cont, local, n_chunks=args.chunks, n_streams=3, task_begin=a, task_end=b)
+    pipe = R.HostPipeline(cont, local, n_chunks=args.chunks, n_streams=args.streams, task_begin=a, task_end=b)
     e2e_times = []
     steps_e2e = max(3, min(args.steps, 20))
     for i in range(args.warmup + steps_e2e):
@@ -533,7 +534,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": int(plan["upload_bytes"]), "d2h_bytes_per_step": int(n_rank),
-                    "chunks": args.chunks, "streams": 3, "kernel_launches_per_step": int(e2e_launches),
+                    "chunks": args.chunks, "streams": args.streams, "kernel_launches_per_step": int(e2e_launches),
                     "note": "recoil_pipeline_run + status per step: host parse + task expansion (a1) per chunk, "
                             "H2D tables + words from pinned memory, kernels, D2H of the symbols to pinned "
                             "memory, 3 streams overlapping; wall clock, max over ranks"},

@@ -238,12 +238,13 @@ int recoil_pipeline_create(const uint8_t *container, uint64_t len, uint64_t task
  * n_streams streams (1 <= n_streams <= 8): one buffer set per stream. */
 int recoil_pipeline_device_bytes(const recoil_pipeline *p, uint32_t n_streams, uint64_t *bytes);
 
-/* One end-to-end decode: per chunk k, on streams[k % n_streams], the host
- * expands the chunk's tasks (a1), then H2D of LUT + task table (from pinned
- * staging) and of the chunk's word slice, the decode kernel, and D2H of the
- * chunk's symbols into host_out[out_lo, out_hi) (absolute symbol indices:
- * host_out is indexed from symbol 0) and of its status word.
- * Copies of one chunk overlap the kernels / copies of the others.  Returns
+/* One end-to-end decode: per chunk k, in device buffer set k % n_streams, the
+ * host expands the chunk's tasks (a1), then H2D of LUT + task table (from
+ * pinned staging) and of the chunk's word slice on streams[0], the decode
+ * kernel on streams[1], and D2H of the chunk's symbols into host_out[out_lo,
+ * out_hi) (absolute symbol indices: host_out is indexed from symbol 0) and of
+ * its status word on streams[2] (with fewer streams the roles share), chained
+ * by events.  Copies in of later chunks overlap copies out of earlier ones.  Returns
  * once everything is enqueued; call recoil_pipeline_status to wait.
  * host_out: N bytes (pinned for asynchronous copies).  Errors: E_ARG, E_CUDA,
  * container errors. */

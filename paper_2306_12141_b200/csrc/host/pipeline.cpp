@@ -3,11 +3,12 @@
 // The task list is cut into contiguous chunks of ~equal committed symbols
 // (the multi-GPU shard plan, §8(e), used here on one device).  For chunk k the
 // host expands its tasks (row a1), stages LUT + task table in pinned memory,
-// and enqueues on stream k % S: H2D of tables and the chunk's word slice,
-// the decode kernel, D2H of the chunk's symbols and of its status word.  With
-// S >= 2 streams the H2D of one chunk, the kernel of another and the D2H of a
-// third overlap (PCIe is full duplex), and the host's a1 work for chunk k+1
-// overlaps the device work of chunk k.
+// and enqueues, into buffer set k % S: the H2D of tables and the chunk's word
+// slice on the copy-in stream, the decode kernel on the compute stream, the
+// D2H of the chunk's symbols and status word on the copy-out stream, chained
+// by events.  The H2D of later chunks overlaps the D2H of earlier ones (PCIe
+// is full duplex), and the host's a1 work for chunk k+1 overlaps the device
+// work of chunk k.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,6 +35,8 @@ struct Pipeline {
   uint8_t *staging[kMaxStreams] = {nullptr};
   uint64_t staging_bytes = 0;
   cudaEvent_t staged[kMaxStreams] = {nullptr};
+  // per buffer set: its H2D done, its kernel done, its D2H done (role streams below)
+  cudaEvent_t ev_in[kMaxStreams] = {nullptr}, ev_k[kMaxStreams] = {nullptr}, ev_out[kMaxStreams] = {nullptr};
   DeviceStatus *status = nullptr;  // pinned, one per chunk
   std::vector<uint64_t> bounds;
   std::vector<Decoder> dec;        // the last run's chunk plans (alive until status)
@@ -42,8 +45,9 @@ struct Pipeline {
   ~Pipeline() {
     for (auto &p : staging)
       if (p) cudaFreeHost(p);
-    for (auto &e : staged)
-      if (e) cudaEventDestroy(e);
+    for (auto *arr : {staged, ev_in, ev_k, ev_out})
+      for (uint32_t i = 0; i < kMaxStreams; ++i)
+        if (arr[i]) cudaEventDestroy(arr[i]);
     if (status) cudaFreeHost(status);
   }
 };
@@ -130,13 +134,20 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (!pl->staging[s] && cudaHostAlloc(reinterpret_cast<void **>(&pl->staging[s]), pl->staging_bytes,
                                            cudaHostAllocDefault) != cudaSuccess)
         return RECOIL_E_CUDA;
-      if (!pl->staged[s] && cudaEventCreateWithFlags(&pl->staged[s], cudaEventDisableTiming) != cudaSuccess)
-        return RECOIL_E_CUDA;
+      for (cudaEvent_t *e : {&pl->staged[s], &pl->ev_in[s], &pl->ev_k[s], &pl->ev_out[s]})
+        if (!*e && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return RECOIL_E_CUDA;
     }
+    // stream roles: copies in on streams[0], kernels on streams[1], copies out on
+    // streams[2] (fewer streams: shared roles).  Chunk k uses buffer set k % n_streams;
+    // the H2D of chunk k waits for the D2H of chunk k - n_streams (same set).  So the
+    // H2D of later chunks overlaps the D2H of earlier ones (PCIe is full duplex).
+    cudaStream_t sh = reinterpret_cast<cudaStream_t>(streams[0]);
+    cudaStream_t sc = reinterpret_cast<cudaStream_t>(streams[std::min<uint32_t>(1, n_streams - 1)]);
+    cudaStream_t so = reinterpret_cast<cudaStream_t>(streams[std::min<uint32_t>(2, n_streams - 1)]);
     std::memset(pl->status, 0, sizeof(DeviceStatus) * pl->chunks);
     for (uint32_t k = 0; k < pl->chunks; ++k) {
       const uint32_t s = k % n_streams;
-      cudaStream_t st = reinterpret_cast<cudaStream_t>(streams[s]);
+      cudaStream_t st = sh;
       Decoder &d = pl->dec[k];
       rc = build_decoder_from(c, pl->bounds[k], pl->bounds[k + 1], &d, true);  // a1 for this chunk
       if (rc) return rc;
@@ -157,6 +168,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (!d.tasks.empty()) std::memcpy(stg + d.tasks_off, d.tasks.data(), sizeof(TaskRec) * d.tasks.size());
       if (!d.heads.empty()) std::memcpy(stg + d.tasks_off, d.heads.data(), sizeof(TaskHead) * d.heads.size());
       const uint64_t staged_bytes = d.fused ? d.rec_off : pn.workspace_bytes;  // raw records: from the container
+      if (k >= n_streams && cudaStreamWaitEvent(sh, pl->ev_out[s], 0) != cudaSuccess) return RECOIL_E_CUDA;
       if (cudaMemcpyAsync(ws, stg, staged_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaEventRecord(pl->staged[s], st) != cudaSuccess)
         return RECOIL_E_CUDA;
@@ -173,13 +185,18 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (pn.word_count > have &&
           cudaMemsetAsync(words + have, 0, 2 * (pn.word_count - have), st) != cudaSuccess)
         return RECOIL_E_CUDA;
-      rc = recoil_decode(reinterpret_cast<recoil_decoder *>(&d), ws, words, dout, st);
+      if (cudaEventRecord(pl->ev_in[s], sh) != cudaSuccess || cudaStreamWaitEvent(sc, pl->ev_in[s], 0) != cudaSuccess)
+        return RECOIL_E_CUDA;
+      rc = recoil_decode(reinterpret_cast<recoil_decoder *>(&d), ws, words, dout, sc);
       if (rc) return rc;
+      if (cudaEventRecord(pl->ev_k[s], sc) != cudaSuccess || cudaStreamWaitEvent(so, pl->ev_k[s], 0) != cudaSuccess)
+        return RECOIL_E_CUDA;
       if (pn.out_hi > pn.out_lo &&
           cudaMemcpyAsync(host_out + pn.out_lo, dout + (pn.out_lo - pn.out_base), pn.out_hi - pn.out_lo,
-                          cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                          cudaMemcpyDeviceToHost, so) != cudaSuccess)
         return RECOIL_E_CUDA;
-      if (cudaMemcpyAsync(&pl->status[k], ws, sizeof(DeviceStatus), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      if (cudaMemcpyAsync(&pl->status[k], ws, sizeof(DeviceStatus), cudaMemcpyDeviceToHost, so) != cudaSuccess ||
+          cudaEventRecord(pl->ev_out[s], so) != cudaSuccess)
         return RECOIL_E_CUDA;
     }
     return RECOIL_OK;

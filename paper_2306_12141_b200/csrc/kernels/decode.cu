@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cstring>
 
 #include "../recoil_internal.h"
@@ -715,13 +717,34 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   const bool adaptive = d->c->adaptive;
   dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive);
   if (d->blocks_per_sm == 0) {
-    int rc = occupancy(fn, dyn_smem(*d), &d->blocks_per_sm);
-    if (rc) return rc;
+    // launch geometry, cached per (device, kernel, dynamic smem) for the process: the
+    // attribute / occupancy queries cost tens of microseconds, and the pipeline builds a
+    // fresh plan per chunk and run
+    struct Geo {
+      int dev;
+      dev::KernelFn fn;
+      size_t dyn;
+      int bps, sms;
+    };
+    static std::mutex mu;
+    static std::vector<Geo> cache;
     int dev_id = 0;
-    if (cudaGetDevice(&dev_id) != cudaSuccess ||
-        cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
-      return RECOIL_E_CUDA;
-    if (d->blocks_per_sm < 1) return RECOIL_E_UNSUPPORTED;  // tables do not fit in shared memory
+    if (cudaGetDevice(&dev_id) != cudaSuccess) return RECOIL_E_CUDA;
+    const size_t dyn = dyn_smem(*d);
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Geo &g : cache)
+      if (g.dev == dev_id && g.fn == fn && g.dyn == dyn) {
+        d->blocks_per_sm = g.bps;
+        d->sm_count = g.sms;
+      }
+    if (d->blocks_per_sm == 0) {
+      int rc = occupancy(fn, dyn, &d->blocks_per_sm);
+      if (rc) return rc;
+      if (cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
+        return RECOIL_E_CUDA;
+      if (d->blocks_per_sm < 1) return RECOIL_E_UNSUPPORTED;  // tables do not fit in shared memory
+      cache.push_back({dev_id, fn, dyn, d->blocks_per_sm, d->sm_count});
+    }
   }
   dev::Params prm;
   prm.lut = reinterpret_cast<const uint8_t *>(ws + d->lut_off);
