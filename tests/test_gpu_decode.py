@@ -255,3 +255,63 @@ def test_config4_combine_65536_to_2048_256_16():
     small = R.recoil_combine_splits(c, 16)
     assert small.tobytes() == oracle.combine(c.tobytes(), 16)
     assert (R.recoil_decode_cpu(small) == sym).all()
+
+
+def test_config5_1GiB_image_residual_bench_launch():
+    """Config 5 per GPU (1 GiB image-residual bytes) with the bench's split rule
+    (2 waves of resident warps), in one launch; sampled tasks against the oracle."""
+    warps, sms = R.recoil_decode_occupancy(0, 11)
+    sym = synth.image_bytes(1 << 30, synth.seed_for(5))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, warps * sms * 2)
+    rc, bad, out, _ = gpu_decode(c)
+    assert rc == 0 and (out == sym).all()
+    _sampled_oracle_tasks(c, out, 8)
+
+
+def test_repeated_decodes_and_concurrent_handles():
+    """One plan decoded repeatedly (status cleared each time) and two handles decoding
+    different containers concurrently on their own streams."""
+    a = synth.text_bytes(2_000_000, 7)
+    b = synth.exp_bytes(3_000_000, 20, 8)
+    ca = R.recoil_encode(a, R.recoil_build_model(synth.histogram(a), 11), 11, 500)
+    cb = R.recoil_encode(b, R.recoil_build_model(synth.histogram(b), 12), 12, 900)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    da, db = R.GpuDecoder(ca, 0, stream=sa), R.GpuDecoder(cb, 0, stream=sb)
+    da.upload()
+    db.upload()
+    for _ in range(3):
+        da.decode()
+        db.decode()
+        assert da.status()[0] == 0 and db.status()[0] == 0
+        assert (da.output().cpu().numpy() == a).all() and (db.output().cpu().numpy() == b).all()
+    da.close()
+    db.close()
+
+
+def test_more_shards_than_tasks():
+    sym = synth.exp_bytes(100_000, 50, 12)
+    c = R.recoil_encode(sym, R.recoil_build_model(synth.histogram(sym), 11), 11, 4)
+    bounds = R.recoil_shard_plan(c, 16)
+    assert bounds[0] == 0 and bounds[-1] == R.recoil_inspect(c)["n_splits"]
+    got = np.zeros(len(sym), dtype=np.uint8)
+    for a, b in zip(bounds, bounds[1:]):
+        rc, bad, out, plan = gpu_decode(c, a, b)
+        assert rc == 0
+        if b > a:
+            got[plan["out_lo"]:plan["out_hi"]] = out
+        else:
+            assert plan["n_tasks"] == 0 and plan["out_hi"] == plan["out_lo"]
+    assert (got == sym).all()
+
+
+@pytest.mark.parametrize("n", list(range(1, 17)))
+def test_every_prob_bits_with_splits(n):
+    """Each kernel instantiation n = 1..16 (packed LUT, split tables) on a split stream."""
+    sym = synth.exp_bytes(700_000, 30, 200 + n)
+    if n < 8:
+        sym = (sym % (1 << max(1, n - 1))).astype(np.uint8)
+    f = R.recoil_build_model(synth.histogram(sym), n)
+    c = R.recoil_encode(sym, f, n, 333)
+    assert c.tobytes() == oracle.recoil_encode(sym, f, n, 333)
+    _check_full(c, sym)

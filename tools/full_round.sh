@@ -11,5 +11,5 @@ for lam in 10 50 200; do timeout 600 python bench.py --config config3 --lam $lam
 for tgt in 2048 256 16; do timeout 600 python bench.py --config config4 --combine-to $tgt --steps 10 --no-extra --no-cpu > gpurun_out/bench_c4_${tgt}_$TAG.json 2> gpurun_out/bench_c4_${tgt}_$TAG.err; done
 timeout 900 python bench.py --config config5 --steps 10 --no-cpu > gpurun_out/bench_c5_$TAG.json 2> gpurun_out/bench_c5_$TAG.err
 for cfg in config1 config3; do timeout 900 ncu --set full --clock-control none -k regex:recoil_decode -s 4 -c 1 -o gpurun_out/prof_${cfg}_$TAG python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu --no-extra > /dev/null 2> gpurun_out/ncu_${cfg}_$TAG.err; done
-tail -3 gpurun_out/smoke_$TAG.log gpurun_out/pytest_full_$TAG.log
+tail -n 3 gpurun_out/smoke_$TAG.log gpurun_out/pytest_full_$TAG.log
 for f in gpurun_out/bench_*_$TAG.json; do echo "== $f"; python -c "import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print(d['value'], d['unit'], d.get('bit_exact'), d['roofline']['frac'], d['config'].get('splits'), d.get('partitioned_baseline',{}).get('value'))" 2>&1 | tail -1; done
