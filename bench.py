@@ -186,10 +186,7 @@ def adaptive_extra(args, local, stream, timed_decode, peak):
     f = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
     models = {"base": h["base"], "len": h["len"], "f": f}
     K = len(h["len"])
-    cbits = 6  # plan.cpp pack_adaptive: the largest coarse table within 40 KB
-    while cbits > 3 and 4 * ((K << cbits) + ((int(f.size) + 3) & ~3) + K) > 40 * 1024:
-        cbits -= 1
-    table_bytes = 4 * ((K << cbits) + ((int(f.size) + 3) & ~3) + K)
+    table_bytes = 4 * ((K << 6) + ((int(f.size) + 3) & ~3) + K)  # plan.cpp pack_adaptive: 64 buckets per model
     warps, sms = R.recoil_decode_occupancy_adaptive(local, table_bytes)
     c = R.recoil_encode_adaptive(sym, mid, models, 16, warps * sms)
     info = R.recoil_inspect(c)

@@ -58,10 +58,9 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
   const uint32_t E = off[K];
   if (E > 65535) return RECOIL_E_UNSUPPORTED;
   const uint32_t Epad = (E + 3) & ~3u;
-  // coarse buckets per model: 2^cbits, the largest (<= 64) whose tables fit
-  // kAdaptiveTableBudget (fewer buckets = longer binary searches)
-  uint32_t cbits = 6;
-  while (cbits > 3 && 4ull * (((uint64_t)K << cbits) + Epad + K) > kAdaptiveTableBudget) --cbits;
+  // 64 coarse buckets per model (a run-time bucket count measured 16 % slower;
+  // 32 buckets at 4 blocks/SM 17 % slower)
+  constexpr uint32_t cbits = 6;
   const uint32_t nbk = 1u << cbits;
   std::vector<uint32_t> w((size_t)K * nbk + Epad + K, 0);
   uint32_t *coarse = w.data(), *ent = w.data() + (size_t)K * nbk, *delta = ent + Epad;
@@ -91,7 +90,7 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
   blob->resize(4 * w.size());
   std::memcpy(blob->data(), w.data(), blob->size());
   *Kout = K;
-  *Eout = E | (cbits << 24);  // E < 2^16; the coarse bucket bits ride in the top byte
+  *Eout = E;
   return RECOIL_OK;
 }
 

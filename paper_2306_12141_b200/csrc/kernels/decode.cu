@@ -179,7 +179,7 @@ struct Warp {
   // adaptive (NB = 0): this lane's model-id slot of the staged block, the
   // model tables (coarse bucket -> entry range, entries F | (f-1) << 16,
   // per-model value offset), n, the coarse shift and the largest model id
-  uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax, cbits;
+  uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax;
   uint32_t gt;       // lanes above this one
   int lane;
   int cursor2;       // 2 x (slice-relative index of the next word to read)
@@ -229,7 +229,7 @@ struct Warp {
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
       const uint32_t slot = x & ((1u << nb) - 1);
-      const uint32_t cb = lds_u32(coarse32 + (((km << cbits) + (slot >> cshift)) << 2));
+      const uint32_t cb = lds_u32(coarse32 + (((km << 6) + (slot >> cshift)) << 2));
       uint32_t lo = cb & 0xFFFFu, hi = cb >> 16;
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
@@ -339,8 +339,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   constexpr int S = sym_bytes<NB>();
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
-    const uint32_t ent_n = p.ad_E & 0xFFFFFFu, cbits = p.ad_E >> 24;
-    const uint32_t words = (p.ad_K << cbits) + ((ent_n + 3) & ~3u) + p.ad_K;
+    const uint32_t words = p.ad_K * 64 + ((p.ad_E + 3) & ~3u) + p.ad_K;
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
@@ -371,12 +370,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   w.lut32 = smem_addr(sm.lut);
   if constexpr (NB == 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
-    w.cbits = p.ad_E >> 24;
     w.coarse32 = smem_addr(sym_dyn);
-    w.ent32 = w.coarse32 + 4 * (p.ad_K << w.cbits);
-    w.delta32 = w.ent32 + 4 * (((p.ad_E & 0xFFFFFFu) + 3) & ~3u);
+    w.ent32 = w.coarse32 + 256 * p.ad_K;
+    w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
     w.nb = p.nbits;
-    w.cshift = p.nbits > w.cbits ? p.nbits - w.cbits : 0;
+    w.cshift = p.nbits > 6 ? p.nbits - 6 : 0;
     w.kmax = p.ad_K - 1;
   }
   if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
@@ -700,12 +698,40 @@ static size_t dyn_smem(const Decoder &d) {  // adaptive: the model tables
   return d.c->adaptive ? d.lut.size() : smem_bytes(d.plan.prob_bits);
 }
 
+// The kernel's dynamic shared-memory limit only ever grows (per device and
+// kernel): launches with less dynamic memory are unaffected by a larger limit,
+// and lowering it would break a cached plan that needs more.
+static int ensure_dyn(dev::KernelFn fn, size_t dyn) {
+  struct Lim {
+    int dev;
+    dev::KernelFn fn;
+    size_t dyn;
+  };
+  static std::mutex mu;
+  static std::vector<Lim> lims;
+  int dev_id = 0;
+  if (cudaGetDevice(&dev_id) != cudaSuccess) return RECOIL_E_CUDA;
+  std::lock_guard<std::mutex> lock(mu);
+  for (Lim &l : lims)
+    if (l.dev == dev_id && l.fn == fn) {
+      if (l.dyn >= dyn) return RECOIL_OK;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
+        return RECOIL_E_CUDA;
+      l.dyn = dyn;
+      return RECOIL_OK;
+    }
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  lims.push_back({dev_id, fn, dyn});
+  return RECOIL_OK;
+}
+
 static int occupancy(dev::KernelFn fn, size_t dyn, int *blocks_per_sm) {
   if (!fn) return RECOIL_E_ARG;
-  cudaError_t e1 = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        (int)cudaSharedmemCarveoutMaxShared);
-  cudaError_t e2 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) return RECOIL_E_CUDA;
+  int rc = ensure_dyn(fn, dyn);
+  if (rc) return rc;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, dev::kThreads, dyn) != cudaSuccess)
     return RECOIL_E_CUDA;
   return RECOIL_OK;
@@ -769,6 +795,10 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.nbits = pl.prob_bits;
   const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
+  if (d->c->adaptive) {  // container-sized tables: the limit may have to grow
+    int rc = ensure_dyn(fn, dyn_smem(*d));
+    if (rc) return rc;
+  }
   fn<<<grid, dev::kThreads, dyn_smem(*d), s>>>(prm);
   return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
 }

@@ -18,7 +18,6 @@ constexpr uint32_t kBlockBytes = 512;    // device output block: 16 groups x 32 
 constexpr uint32_t kMaxGpuProbBits = 16; // GPU decode: packed u32 LUT up to n = 12, split tables above
 constexpr uint32_t kNoFinals = 0xFFFFFFFFu;
 constexpr int64_t kNoEndCheck = INT64_MIN;
-constexpr uint64_t kAdaptiveTableBudget = 40 * 1024;  // adaptive model tables in smem (64 buckets for K = 64: 3 blocks / SM; 32 buckets + 4 blocks measured 17 % slower)
 
 // Parsed container of either kind. Recoil: M tasks, M-1 split points.
 // Partitioned: M partitions (tasks), no points.
@@ -126,10 +125,9 @@ void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
 void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,
                         uint64_t *bounds);
 void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
-// Adaptive model tables for the GPU: K x 2^cbits coarse buckets
-// (lo | hi << 16 entry range; cbits <= 6, the largest within
-// kAdaptiveTableBudget), E entries F | (f-1) << 16 (padded to 4), K value
-// offsets.  *E = entries | cbits << 24.  E_UNSUPPORTED if entries > 65535.
+// Adaptive model tables for the GPU: K x 64 coarse buckets
+// (lo | hi << 16 entry range), E entries F | (f-1) << 16 (padded to 4), K
+// value offsets.  E_UNSUPPORTED if E > 65535.
 int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
 
 
