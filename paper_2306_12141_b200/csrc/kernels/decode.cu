@@ -337,6 +337,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
 
   constexpr int S = sym_bytes<NB>();
+  // the first task's head is requested before the LUT staging, so its latency
+  // overlaps the block's LUT copy (fused plans)
+  uint32_t hw_first = 0;
+  if constexpr (FUSED) {
+    const uint32_t t0 = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    hw_first = t0 < p.n_tasks ? __ldg(reinterpret_cast<const uint32_t *>(&p.heads[t0]) + (threadIdx.x & 7)) : 0u;
+  }
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
     const uint32_t words = p.ad_K * 64 + ((p.ad_E + 3) & ~3u) + p.ad_K;
@@ -423,9 +430,18 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   int buf = 0;
   if (t < p.n_tasks) {
     issue_task(t, 0);
-    load_head(t);
+    if constexpr (FUSED) hw = hw_first;
     load_windows();
   }
+  // a7: the task's word window: chunks c, c-1, c-2 resident, c-3 in flight
+  auto issue_window = [&](int32_t cursor0) {
+    w.cursor2 = 2 * cursor0;
+    w.cchunk = cursor0 >> 8;
+    w.issue_chunk(w.cchunk);
+    w.issue_chunk(w.cchunk - 1);
+    w.issue_chunk(w.cchunk - 2);
+    w.issue_chunk(w.cchunk - 3);
+  };
   while (t < p.n_tasks) {
     cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
@@ -438,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       // tab:metadata_codec): anchor state and group of every lane, the sync starts
       // (min anchor index) that bound this task's committed range (reading Z13)
       cursor0 = (int32_t)__shfl_sync(kFull, hw, 0);
+      issue_window(cursor0);  // before the record expansion: the copies overlap it
       start_group = (int32_t)__shfl_sync(kFull, hw, 1);
       const uint32_t rec = __shfl_sync(kFull, hw, 2), rec_prev = __shfl_sync(kFull, hw, 3);
       const uint32_t maxg_prev = __shfl_sync(kFull, hw, 4), flags = __shfl_sync(kFull, hw, 5);
@@ -497,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       init_group = start_group - (int32_t)(lw >> 16);
       cursor0 = (int)r.cursor0;
       __syncwarp();
+      issue_window(cursor0);
     }
     // next task: 0 = not asked, 1 = atomic in flight, 2 = record / head in flight,
     // 3 = (fused) record windows in flight
@@ -517,13 +535,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       }
     };
 
-    // a7: word window -- chunks c, c-1, c-2 resident, c-3 in flight
-    w.cursor2 = 2 * cursor0;
-    w.cchunk = cursor0 >> 8;
-    w.issue_chunk(w.cchunk);
-    w.issue_chunk(w.cchunk - 1);
-    w.issue_chunk(w.cchunk - 2);
-    w.issue_chunk(w.cchunk - 3);
+    // a7: word window (issued above) -- chunks c, c-1, c-2 resident, c-3 in flight
     cp_wait<1>();
     __syncwarp();
 
