@@ -58,12 +58,14 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
   const uint32_t E = off[K];
   if (E > 65535) return RECOIL_E_UNSUPPORTED;
   const uint32_t Epad = (E + 3) & ~3u;
-  // 64 coarse buckets per model (a run-time bucket count measured 16 % slower;
-  // 32 buckets at 4 blocks/SM 17 % slower)
-  constexpr uint32_t cbits = 6;
-  const uint32_t nbk = 1u << cbits;
-  std::vector<uint32_t> w((size_t)K * nbk + Epad + K, 0);
-  uint32_t *coarse = w.data(), *ent = w.data() + (size_t)K * nbk, *delta = ent + Epad;
+  // 64 coarse buckets per model: the u16 entry index containing each bucket's
+  // first slot, 65 boundaries (+1 pad) per model; bucket b's entries lie in
+  // [lo[b], lo[b+1]] (a superset by at most one entry, excluded by the search)
+  constexpr uint32_t cbits = 6, nbk = 1u << cbits, crow = nbk + 2;
+  const size_t cwords = ((size_t)K * crow * 2 + 15) / 16 * 4;  // u16 rows, 16-B aligned
+  std::vector<uint32_t> w(cwords + Epad + K, 0);
+  uint16_t *coarse = reinterpret_cast<uint16_t *>(w.data());
+  uint32_t *ent = w.data() + cwords, *delta = ent + Epad;
   const uint32_t shift = n > cbits ? n - cbits : 0, nb = 1u << (n - shift);
   std::vector<uint32_t> F;
   for (uint32_t k = 0; k < K; ++k) {
@@ -81,11 +83,8 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
       uint32_t j = (uint32_t)(std::upper_bound(F.begin(), F.end(), slot) - F.begin());
       return off[k] + (j ? j - 1 : 0);
     };
-    for (uint32_t b = 0; b < nbk; ++b) {
-      const uint32_t bb = std::min(b, nb - 1);
-      const uint32_t s0 = bb << shift, s1 = ((bb + 1) << shift) - 1;
-      coarse[k * nbk + b] = entry_of(s0) | (entry_of(s1) << 16);
-    }
+    for (uint32_t b = 0; b <= nbk; ++b)
+      coarse[k * crow + b] = (uint16_t)(b < nb ? entry_of(b << shift) : off[k] + keep[k] - 1);
   }
   blob->resize(4 * w.size());
   std::memcpy(blob->data(), w.data(), blob->size());

@@ -51,7 +51,7 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 // NB = 0 is the adaptive codec (NEXT rows 1 + 4: index-keyed models, 16-bit
 // symbols, n at run time); its model tables live in dynamic shared memory.
 template <int NB>
-__host__ __device__ constexpr int min_blocks() { return NB == 0 ? 3 : NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
+__host__ __device__ constexpr int min_blocks() { return NB == 0 ? 4 : NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
 template <int NB>
 __host__ __device__ constexpr int sym_bytes() { return NB == 0 ? 2 : 1; }
 constexpr int kRingChunks = 4;
@@ -229,8 +229,8 @@ struct Warp {
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
       const uint32_t slot = x & ((1u << nb) - 1);
-      const uint32_t cb = lds_u32(coarse32 + (((km << 6) + (slot >> cshift)) << 2));
-      uint32_t lo = cb & 0xFFFFu, hi = cb >> 16;
+      const uint32_t ca = coarse32 + 2 * (km * 66 + (slot >> cshift));
+      uint32_t lo = lds_u16(ca), hi = lds_u16(ca + 2);
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
           const uint32_t m = (lo + hi + 1) >> 1;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   }
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
-    const uint32_t words = p.ad_K * 64 + ((p.ad_E + 3) & ~3u) + p.ad_K;
+    const uint32_t words = (p.ad_K * 66 * 2 + 15) / 16 * 4 + ((p.ad_E + 3) & ~3u) + p.ad_K;
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   if constexpr (NB == 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
-    w.ent32 = w.coarse32 + 256 * p.ad_K;
+    w.ent32 = w.coarse32 + (p.ad_K * 66 * 2 + 15) / 16 * 16;
     w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
     w.nb = p.nbits;
     w.cshift = p.nbits > 6 ? p.nbits - 6 : 0;

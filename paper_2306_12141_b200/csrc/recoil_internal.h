@@ -125,9 +125,10 @@ void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
 void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,
                         uint64_t *bounds);
 void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
-// Adaptive model tables for the GPU: K x 64 coarse buckets
-// (lo | hi << 16 entry range), E entries F | (f-1) << 16 (padded to 4), K
-// value offsets.  E_UNSUPPORTED if E > 65535.
+// Adaptive model tables for the GPU: K x 66 u16 coarse bucket
+// boundaries (entry holding each of the 64 buckets' first slot, + end, + pad;
+// 16-B aligned), E entries F | (f-1) << 16 (padded to 4), K value offsets.
+// E_UNSUPPORTED if E > 65535.
 int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
 
 
