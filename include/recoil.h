@@ -170,6 +170,16 @@ typedef struct {
  * 2^31 words or more). */
 int recoil_decoder_create(const uint8_t *container, uint64_t len, uint64_t task_begin,
                           uint64_t task_end, recoil_decoder **out);
+
+/* Decoder-side combine (P:266-272 on the client): plan the decode with only
+ * the split points recoil_combine_splits(container, target_splits) would keep
+ * (1-based positions k, 2k, ..., k = ceil(M / target_splits)), reading the
+ * kept records in place -- no rewritten container, no copy of the word
+ * stream.  Output identical to decoding the combined container; task indices
+ * refer to the kept splits.  Errors as recoil_decoder_create; E_ARG for a
+ * partitioned container. */
+int recoil_decoder_create_subset(const uint8_t *container, uint64_t len, uint32_t target_splits,
+                                 uint64_t task_begin, uint64_t task_end, recoil_decoder **out);
 int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan);
 
 /* Asynchronous host->device copy on cuda_stream of the packed LUT and task

@@ -348,6 +348,47 @@ extern "C" int recoil_decoder_create(const uint8_t *container, uint64_t len, uin
   }
 }
 
+extern "C" int recoil_decoder_create_subset(const uint8_t *container, uint64_t len, uint32_t target_splits,
+                                            uint64_t task_begin, uint64_t task_end, recoil_decoder **out) {
+  if (!container || !out || target_splits < 1) return RECOIL_E_ARG;
+  *out = nullptr;
+  try {
+    auto full = std::make_shared<Container>();
+    int rc = parse_container(container, len, full.get(), /*light=*/true);
+    if (rc) return rc;
+    if (full->partitioned) return RECOIL_E_ARG;  // partitions cannot be combined
+    // the view: the split points recoil_combine_splits would keep (1-based positions
+    // k, 2k, ... with k = ceil(M / target), Z11/Z12), over the same container bytes
+    auto view = std::make_shared<Container>(*full);
+    if (target_splits < full->M) {
+      const uint64_t P = full->M - 1, k = ceil_div(full->M, target_splits);
+      view->offset.clear();
+      view->maxg.clear();
+      view->rec_off.clear();
+      for (uint64_t pos = k; pos <= P; pos += k) {
+        view->offset.push_back(full->offset[pos - 1]);
+        view->maxg.push_back(full->maxg[pos - 1]);
+        view->rec_off.push_back(full->rec_off[pos - 1]);
+      }
+      view->M = (uint32_t)view->offset.size() + 1;
+      // rec_off[k + 1] bounds record k's bytes (here: the next kept record, a
+      // looser but valid bound); the last bound is the last kept record's end
+      const uint64_t last = view->offset.empty() ? 0 : (P / k) * k;
+      view->rec_off.push_back(view->offset.empty() ? full->rec_off[0] : full->rec_off[last]);
+    }
+    Decoder *d = new Decoder();
+    rc = build_decoder_from(view, task_begin, task_end, d, true);
+    if (rc) {
+      delete d;
+      return rc;
+    }
+    *out = reinterpret_cast<recoil_decoder *>(d);
+    return RECOIL_OK;
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}
+
 extern "C" int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan) {
   if (!dec || !plan) return RECOIL_E_ARG;
   *plan = reinterpret_cast<const Decoder *>(dec)->plan;

@@ -34,7 +34,7 @@ EXPORTS = [
     "recoil_decode_occupancy", "recoil_shard_plan", "recoil_decode_cpu", "recoil_decode_cpu_ex", "recoil_cpu_simd",
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
     "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
-    "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive",
+    "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive", "recoil_decoder_create_subset",
 ]
 
 
@@ -105,6 +105,7 @@ def load(path: str = LIB_PATH):
         "recoil_encode_adaptive": (i32, [P, u64, P, u32, P, P, P, u32, u32, P, P]),
         "recoil_decode_adaptive": (i32, [P, P, P, P, P, P]),
         "recoil_decode_occupancy_adaptive": (i32, [i32, u64, P, P]),
+        "recoil_decoder_create_subset": (i32, [P, u64, u32, u64, u64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -231,6 +232,15 @@ def recoil_decoder_create(container, task_begin: int = 0, task_end: int = (1 << 
     return h
 
 
+def recoil_decoder_create_subset(container, target_splits: int, task_begin: int = 0,
+                                 task_end: int = (1 << 64) - 1) -> ctypes.c_void_p:
+    c = _u8(container)
+    h = ctypes.c_void_p()
+    _check(load().recoil_decoder_create_subset(c.ctypes.data, c.size, target_splits, task_begin, task_end,
+                                               ctypes.byref(h)), "recoil_decoder_create_subset")
+    return h
+
+
 def recoil_decoder_plan(handle) -> dict:
     p = recoil_plan()
     _check(load().recoil_decoder_plan(handle, ctypes.byref(p)), "recoil_decoder_plan")
@@ -297,11 +307,12 @@ class GpuDecoder:
     """
 
     def __init__(self, container, device: int = 0, task_begin: int = 0, task_end: int = (1 << 64) - 1,
-                 stream=None):
+                 stream=None, subset: int | None = None):
         import torch
         self.container = _u8(container)
         self.device = torch.device("cuda", device)
-        self.handle = recoil_decoder_create(self.container, task_begin, task_end)
+        self.handle = (recoil_decoder_create(self.container, task_begin, task_end) if subset is None else
+                       recoil_decoder_create_subset(self.container, subset, task_begin, task_end))
         self.plan = recoil_decoder_plan(self.handle)
         p = self.plan
         self.stream = stream or torch.cuda.current_stream(self.device)

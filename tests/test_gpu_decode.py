@@ -344,3 +344,19 @@ def test_fuzzed_containers_never_fault_or_hang():
         dec.close()
     torch.cuda.synchronize()
     assert sum(outcomes.values()) == 60, outcomes
+
+
+@pytest.mark.parametrize("target", [2048, 300, 16, 1])
+def test_decoder_side_combine(target):
+    """Decoder-adaptive scalability on the client: decode with a subset of
+    the split points in place == decode of the combined container == the input."""
+    sym = synth.exp_bytes(8_000_000, 50, 21)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 8192)
+    dec = R.GpuDecoder(c, 0, subset=target)
+    dec.upload()
+    dec.decode()
+    assert dec.status()[0] == 0
+    assert dec.plan["n_tasks"] == R.recoil_inspect(R.recoil_combine_splits(c, target))["n_splits"]
+    assert (dec.output().cpu().numpy() == sym).all()
+    dec.close()

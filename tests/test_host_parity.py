@@ -327,3 +327,21 @@ def test_adaptive_quantize_and_errors():
     with pytest.raises(R.RecoilError) as e:
         R.recoil_decode_cpu(c)
     assert e.value.rc == R.RECOIL_E_UNSUPPORTED
+
+
+def test_decoder_side_combine_plans_equal_combined_containers():
+    """recoil_decoder_create_subset plans exactly what decoding recoil_combine_splits' output plans."""
+    sym = synth.exp_bytes(2_000_000, 50, 3)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 1000)
+    keys = ("n_tasks", "word_lo", "word_count", "out_lo", "out_hi", "out_base", "out_count")
+    for target in (5000, 1000, 999, 300, 17, 2, 1):
+        h = R.recoil_decoder_create_subset(c, target)
+        p = R.recoil_decoder_plan(h)
+        R.recoil_decoder_destroy(h)
+        h2 = R.recoil_decoder_create(R.recoil_combine_splits(c, target))
+        p2 = R.recoil_decoder_plan(h2)
+        R.recoil_decoder_destroy(h2)
+        assert all(p[k] == p2[k] for k in keys), target
+    with pytest.raises(R.RecoilError):
+        R.recoil_decoder_create_subset(R.recoil_partitioned_encode(sym, f, 11, 8), 2)
