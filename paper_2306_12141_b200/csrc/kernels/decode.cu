@@ -38,20 +38,40 @@
 namespace recoil {
 namespace dev {
 
-constexpr int kWarpsPerBlock = 8;
-constexpr int kThreads = kWarpsPerBlock * 32;
-// Resident blocks per SM the kernel is compiled for.  The steady state is bound
-// by the latency of its per-group dependency chain, so more warps help: n <= 11
-// runs 6 blocks (48 warps, 40 registers; 7 blocks at 32 registers measured
-// 11 % slower, 5 blocks 6 % slower); n = 12 (16 KB LUT) and n >= 13 (up to
-// 64 KB symbol table) are shared-memory limited and keep 48 registers.
-#ifndef RECOIL_MIN_BLOCKS
-#define RECOIL_MIN_BLOCKS 6
+// Warps per block.  The SM's warp schedulers favour older CTAs: with one task
+// per warp, the warps of the last-resident CTA get issue slots only when the
+// others stall and finish last (measured per task with -DRECOIL_TIMELINE: CTA
+// rank 0..5 of an SM at 8 warps took 55 / 59 / 66 / 77 / 90 / 101 us of a 104 us
+// decode, warps of one CTA alike).  So the static kernels run 2 CTAs of 24 warps
+// (48 warps per SM, two priority levels; config 2: 989 -> 1082 GB/s, config 3
+// 1277 -> 1324); the adaptive kernel, whose model tables take 23 KB more per
+// CTA, keeps 8-warp CTAs (4 per SM).
+#ifndef RECOIL_WARPS
+#define RECOIL_WARPS 24
+#endif
+#ifndef RECOIL_WARPS_ADAPTIVE
+#define RECOIL_WARPS_ADAPTIVE 8
+#endif
+template <int NB>
+__host__ __device__ constexpr int warps_per_block() { return NB == 0 ? RECOIL_WARPS_ADAPTIVE : RECOIL_WARPS; }
+template <int NB>
+__host__ __device__ constexpr int threads_per_block() { return 32 * warps_per_block<NB>(); }
+// Resident warps per SM the register budget is sized for.  The steady state is
+// bound by the shared-memory pipe and the latency of the per-group dependency
+// chain, so more warps help: n <= 12 runs 48 warps (2 CTAs, 40 registers; at 8-warp
+// CTAs, 56 warps at 32 registers measured 11 % slower, 40 warps 6 % slower);
+// n >= 13 (up to 64 KB symbol table) is shared-memory limited to one CTA.
+#ifndef RECOIL_MIN_WARPS
+#define RECOIL_MIN_WARPS 48
 #endif
 // NB = 0 is the adaptive codec (NEXT rows 1 + 4: index-keyed models, 16-bit
 // symbols, n at run time); its model tables live in dynamic shared memory.
 template <int NB>
-__host__ __device__ constexpr int min_blocks() { return NB == 0 ? 4 : NB <= 11 ? RECOIL_MIN_BLOCKS : 5; }
+__host__ __device__ constexpr int min_blocks() {
+  constexpr int w = warps_per_block<NB>();
+  return NB == 0 ? (32 / w > 0 ? 32 / w : 1) : NB <= 12 ? (RECOIL_MIN_WARPS / w > 0 ? RECOIL_MIN_WARPS / w : 1)
+                                                       : (40 / w > 0 ? 40 / w : 1);
+}
 template <int NB>
 __host__ __device__ constexpr int sym_bytes() { return NB == 0 ? 2 : 1; }
 constexpr int kRingChunks = 4;
@@ -83,24 +103,38 @@ struct Params {
   uint32_t ad_K, ad_E, nbits;
 };
 
-// Static shared memory per block (about 33 KB for n = 11): the word rings need
-// 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
+// Shared memory per block (dynamic; about 31 KB for n = 11 at 8 warps): the word
+// rings need 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
 constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 template <int NB>
-struct __align__(16) Smem {
-  // Order matters: the CTA's static shared memory starts 1 KB into its shared
-  // window (the reserved system area), so stage + rec (7 KB) put the LUT on an
-  // 8 KB boundary, and a LUT of <= 8 KB (n <= 11) is addressed with one LOP3:
-  // base | ((x << 2) & mask).  The LUT is at least 2 KB, so the word rings
-  // after it start 2 KB-aligned (ring addresses are base | (pos & 0x7FE)).
-  // Both alignments are checked at kernel start.
-  uint8_t stage[kWarpsPerBlock][kBlockBytes * sym_bytes<NB>()];  // 8 x 512 symbols output staging
-  TaskRec rec[kWarpsPerBlock][2];              // current / next task record
-  // n <= 12: packed LUT s | bias << 8 | f << 20.  n >= 13 (NEXT row 1):
-  // f and F per symbol here, the 2^n slot -> symbol bytes in dynamic smem.
-  // NB = 0 (adaptive): the model ids of each warp's current output block (8 x 512 B).
-  uint32_t lut[NB == 0 ? 1024 : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512];
-  uint16_t ring[kWarpsPerBlock][kRingWords];   // 8 x 2 KB word windows
+__host__ __device__ constexpr int lut_words() {
+  return NB == 0 ? 128 * warps_per_block<0>() : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512;
+}
+// bytes before the LUT: staging + records, padded to 7 KB mod 8 KB (see Smem)
+constexpr int kPreLut(int W, int S) { return W * ((int)kBlockBytes * S + 2 * (int)sizeof(TaskRec)); }
+constexpr int kLutPad(int W, int S) { return ((7168 - kPreLut(W, S) % 8192) % 8192 + 8192) % 8192; }
+// Block layout (byte offsets into the dynamic shared memory).  Order matters: the
+// CTA's shared memory starts 1 KB into its shared window (the reserved system
+// area), so stage + rec + pad (7 KB mod 8 KB) put the LUT on an 8 KB boundary,
+// and a LUT of <= 8 KB (n <= 11) is addressed with one LOP3: base | ((x << 2) &
+// mask).  The LUT is at least 2 KB, so the word rings after it start 2 KB-aligned
+// (ring addresses are base | (pos & 0x7FE)).  Both alignments are checked at
+// kernel start.
+//   stage[W][512 S]  per warp 512 symbols of output staging
+//   rec[W][2]        current / next task record (prebuilt-record plans)
+//   lut[lut_words]   n <= 12: packed LUT s | bias << 8 | f << 20; n >= 13
+//                    (NEXT row 1): f and F per symbol (the 2^n slot -> symbol bytes
+//                    follow the layout); adaptive: each warp's staged model ids
+//   ring[W][1024]    per warp 2 KB word window (u16)
+template <int NB>
+struct Smem {
+  static constexpr int S = sym_bytes<NB>();
+  static constexpr int W = warps_per_block<NB>();
+  static constexpr int kStage = 0;
+  static constexpr int kRec = kStage + W * (int)kBlockBytes * S;
+  static constexpr int kLut = kRec + W * 2 * (int)sizeof(TaskRec) + kLutPad(W, S);
+  static constexpr int kRing = kLut + 4 * lut_words<NB>();
+  static constexpr int kBytes = kRing + W * 2 * kRingWords;
 };
 constexpr int kOrLutMaxBits = 11;  // LUT base alignment trick up to 8 KB
 
@@ -151,6 +185,22 @@ __device__ __forceinline__ uint32_t lanemask_gt() {
   return m;
 }
 
+#ifdef RECOIL_TIMELINE
+// Experiment builds only (tools/build_variant.sh -DRECOIL_TIMELINE): per task the
+// %globaltimer at its start and end, the SM and the warp's kernel start time.
+constexpr uint32_t kTimelineMax = 1u << 17;
+__device__ unsigned long long g_timeline[kTimelineMax][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+#endif
 // 4 bytes at byte offset `off` of a warp-distributed window (lane k holds bytes
 // [4k, 4k + 4) of it, little endian); off + 4 <= 128.
 __device__ __forceinline__ uint32_t window_u32(uint32_t win, uint32_t off) {
@@ -332,11 +382,19 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
 }
 
 template <int NB, bool FUSED>
-__global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kernel(const Params p) {
-  __shared__ Smem<NB> sm;
-  extern __shared__ __align__(16) uint8_t sym_dyn[];  // n >= 13 only: 2^n slot -> symbol
+__global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) recoil_decode_kernel(const Params p) {
+  constexpr int kWarpsPerBlock = warps_per_block<NB>();
+  constexpr int kThreads = threads_per_block<NB>();
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  using L = Smem<NB>;
+  uint32_t *const sm_lut = reinterpret_cast<uint32_t *>(smem_dyn + L::kLut);
+  TaskRec *const sm_rec = reinterpret_cast<TaskRec *>(smem_dyn + L::kRec);  // [warp][2]
+  uint8_t *const sym_dyn = smem_dyn + L::kBytes;  // n >= 13: 2^n slot -> symbol; adaptive: model tables
 
   constexpr int S = sym_bytes<NB>();
+#ifdef RECOIL_TIMELINE
+  const unsigned long long tl_kernel = gtime();
+#endif
   // the first task's head is requested before the LUT staging, so its latency
   // overlaps the block's LUT copy (fused plans)
   uint32_t hw_first = 0;
@@ -355,14 +413,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     constexpr uint32_t kWords = 1u << NB;
     if (kWords >= 4) {
       for (uint32_t i = threadIdx.x; i < kWords / 4; i += kThreads)
-        reinterpret_cast<int4 *>(sm.lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
+        reinterpret_cast<int4 *>(sm_lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     } else if (threadIdx.x < kWords) {
-      sm.lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut)[threadIdx.x];
+      sm_lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut)[threadIdx.x];
     }
   } else {
     for (uint32_t i = threadIdx.x; i < (1u << NB) / 16; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
-    sm.lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut + (1u << NB))[threadIdx.x];
+    if (threadIdx.x < 256) sm_lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut + (1u << NB))[threadIdx.x];
   }
   __syncthreads();
 
@@ -371,10 +429,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
   w.lane = threadIdx.x & 31;
   const int lane = w.lane;
   const int warp = threadIdx.x >> 5;
-  w.ring32 = smem_addr(&sm.ring[warp][0]);
-  w.stage32 = smem_addr(&sm.stage[warp][S * lane]);
+  w.ring32 = smem_addr(smem_dyn + L::kRing + warp * 2 * kRingWords);
+  w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
   w.gt = lanemask_gt();
-  w.lut32 = smem_addr(sm.lut);
+  w.lut32 = smem_addr(sm_lut);
   if constexpr (NB == 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
@@ -390,8 +448,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     return;
   }
   w.cchunk = 0;
-  const uint32_t rec32 = smem_addr(&sm.rec[warp][0]);
-  const uint32_t *lut = sm.lut;
+  const uint32_t rec32 = smem_addr(&sm_rec[2 * warp]);
+  const uint32_t *lut = sm_lut;
   const uint8_t *sym = sym_dyn;
 
   // a3: persistent warps.  The first wave of task ids is static; afterwards a
@@ -443,6 +501,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     w.issue_chunk(w.cchunk - 3);
   };
   while (t < p.n_tasks) {
+#ifdef RECOIL_TIMELINE
+    const unsigned long long tl_start = gtime();
+#endif
     cp_wait<0>();  // this task's record and any window copy still in flight have landed
     __syncwarp();
     int32_t start_group, init_group, cursor0;
@@ -474,10 +535,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
         const uint32_t d = series_elem(pf_se, (rec + 64) & 3u, lane, &w);  // anchor - group
         bad_meta |= d > (uint32_t)start_group;
         init_group = start_group - (int32_t)d;
-        int32_t idx = init_group * 32 + lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
-        ss_t = idx;
+        // sync start = min_j (32 group_j + j) = 32 start_group + 31 - max_j (32 d_j + 31 - j):
+        // one REDUX on a small non-negative key (d < 2^16), exact for any N
+        ss_t = 32 * (int64_t)start_group + 31 - (int64_t)__reduce_max_sync(kFull, 32 * d + 31 - lane);
         whi = (uint64_t)(ss_t / 32 + 1) * 32;
       }
       if (flags & kHeadFirst) {
@@ -487,10 +547,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
         uint32_t w;
         const uint32_t d = series_elem(pf_pr, (rec_prev + 64) & 3u, lane, &w);
         bad_meta |= d > maxg_prev;
-        int32_t idx = ((int32_t)maxg_prev - (int32_t)d) * 32 + lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(kFull, idx, o));
-        lo = (uint64_t)idx;
+        lo = 32 * (uint64_t)maxg_prev + 31 - __reduce_max_sync(kFull, 32 * d + 31 - lane);
         end_cursor = kNoEndCheck;
         bad_meta |= (int64_t)lo >= ss_t;  // sync starts strictly increasing
       }
@@ -503,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
         start_group = -1;
       }
     } else {
-      const TaskRec &r = sm.rec[warp][buf];
+      const TaskRec &r = sm_rec[2 * warp + buf];
       start_group = r.start_group;
       lo = r.commit_lo;
       whi = r.write_hi;
@@ -540,14 +597,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
     __syncwarp();
 
     const int32_t lo_group = (int32_t)(lo >> 5);
-    int32_t min_init = init_group;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) min_init = min(min_init, __shfl_xor_sync(kFull, min_init, o));
+    const int32_t min_init = __reduce_min_sync(kFull, init_group);
     const int32_t g_sync_end = max(min_init, lo_group);
     // 32-bit output bookkeeping relative to the block of lo_group (bytes: S per symbol)
     const int32_t b_lo = lo_group >> 4;
     uint8_t *const out_blo = p.out + ((uint64_t)b_lo * kBlockBytes - p.out_base) * S;
-    const int woff = (lo_group * (int)kLanes - b_lo * (int)kBlockBytes) * S;  // 0..511 symbols
+    const int woff = (lo_group & 15) * (int)kLanes * S;  // 0..511 symbols into block b_lo
     const int wend = (int)(whi - (uint64_t)b_lo * kBlockBytes) * S;
     constexpr int kBlk = (int)kBlockBytes * S;  // output block bytes
 
@@ -652,6 +707,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NB>()) recoil_decode_kern
       atomicOr(&p.status->flags, (under ? 1u : 0u) | (bad_end ? 2u : 0u));
       atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
     }
+#ifdef RECOIL_TIMELINE
+    if (lane == 0 && task_id < kTimelineMax) {
+      g_timeline[task_id][0] = tl_start;
+      g_timeline[task_id][1] = gtime();
+      g_timeline[task_id][2] = smid() | (uint64_t)(blockIdx.x * kWarpsPerBlock + warp) << 16;
+      g_timeline[task_id][3] = tl_kernel;
+    }
+#endif
     t = t_next;
     buf ^= 1;
   }
@@ -703,11 +766,20 @@ static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false) {
 
 }  // namespace dev
 
-static size_t smem_bytes(uint32_t nbits) {  // dynamic part only: the slot -> symbol table for n >= 13
-  return nbits > (uint32_t)dev::kNarrowMaxBits ? (size_t)1 << nbits : 0;
+static size_t layout_bytes(uint32_t nbits) {  // dev::Smem<n>::kBytes (n = 0: adaptive)
+  switch (nbits) {
+    case 0: return dev::Smem<0>::kBytes;
+    case 10: return dev::Smem<10>::kBytes;
+    case 11: return dev::Smem<11>::kBytes;
+    case 12: return dev::Smem<12>::kBytes;
+    default: return nbits <= 9 ? dev::Smem<9>::kBytes : dev::Smem<13>::kBytes;
+  }
 }
-static size_t dyn_smem(const Decoder &d) {  // adaptive: the model tables
-  return d.c->adaptive ? d.lut.size() : smem_bytes(d.plan.prob_bits);
+static size_t smem_bytes(uint32_t nbits) {  // the block layout + the slot -> symbol table for n >= 13
+  return layout_bytes(nbits) + (nbits > (uint32_t)dev::kNarrowMaxBits ? (size_t)1 << nbits : 0);
+}
+static size_t dyn_smem(const Decoder &d) {  // adaptive: the layout + the model tables
+  return d.c->adaptive ? layout_bytes(0) + d.lut.size() : smem_bytes(d.plan.prob_bits);
 }
 
 // The kernel's dynamic shared-memory limit only ever grows (per device and
@@ -740,11 +812,11 @@ static int ensure_dyn(dev::KernelFn fn, size_t dyn) {
   return RECOIL_OK;
 }
 
-static int occupancy(dev::KernelFn fn, size_t dyn, int *blocks_per_sm) {
+static int occupancy(dev::KernelFn fn, int threads, size_t dyn, int *blocks_per_sm) {
   if (!fn) return RECOIL_E_ARG;
   int rc = ensure_dyn(fn, dyn);
   if (rc) return rc;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, dev::kThreads, dyn) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, threads, dyn) != cudaSuccess)
     return RECOIL_E_CUDA;
   return RECOIL_OK;
 }
@@ -754,6 +826,7 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   const recoil_plan &pl = d->plan;
   const bool adaptive = d->c->adaptive;
   dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive);
+  const int warps = adaptive ? dev::warps_per_block<0>() : dev::warps_per_block<11>();
   if (d->blocks_per_sm == 0) {
     // launch geometry, cached per (device, kernel, dynamic smem) for the process: the
     // attribute / occupancy queries cost tens of microseconds, and the pipeline builds a
@@ -776,7 +849,7 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
         d->sm_count = g.sms;
       }
     if (d->blocks_per_sm == 0) {
-      int rc = occupancy(fn, dyn, &d->blocks_per_sm);
+      int rc = occupancy(fn, 32 * warps, dyn, &d->blocks_per_sm);
       if (rc) return rc;
       if (cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev_id) != cudaSuccess)
         return RECOIL_E_CUDA;
@@ -805,13 +878,13 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.ad_K = d->ad_K;
   prm.ad_E = d->ad_E;
   prm.nbits = pl.prob_bits;
-  const uint32_t need = (pl.n_tasks + dev::kWarpsPerBlock - 1) / dev::kWarpsPerBlock;
+  const uint32_t need = (pl.n_tasks + warps - 1) / warps;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
   if (d->c->adaptive) {  // container-sized tables: the limit may have to grow
     int rc = ensure_dyn(fn, dyn_smem(*d));
     if (rc) return rc;
   }
-  fn<<<grid, dev::kThreads, dyn_smem(*d), s>>>(prm);
+  fn<<<grid, 32 * warps, dyn_smem(*d), s>>>(prm);
   return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
 }
 
@@ -914,12 +987,12 @@ extern "C" int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0;
-  int rc = occupancy(dev::kernel_for(16, true, true), (size_t)table_bytes, &per_sm);
+  int rc = occupancy(dev::kernel_for(16, true, true), dev::threads_per_block<0>(), layout_bytes(0) + (size_t)table_bytes, &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;
   if (e2 != cudaSuccess) return RECOIL_E_CUDA;
-  if (warps_per_sm) *warps_per_sm = per_sm * dev::kWarpsPerBlock;
+  if (warps_per_sm) *warps_per_sm = per_sm * dev::warps_per_block<0>();
   if (sm_count) *sm_count = sms;
   return RECOIL_OK;
 }
@@ -930,12 +1003,19 @@ extern "C" int recoil_decode_occupancy(int device, uint32_t nbits, int *warps_pe
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0;
-  int rc = occupancy(dev::kernel_for(nbits, true), smem_bytes(nbits), &per_sm);
+  int rc = occupancy(dev::kernel_for(nbits, true), dev::threads_per_block<11>(), smem_bytes(nbits), &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;
   if (e2 != cudaSuccess) return RECOIL_E_CUDA;
-  if (warps_per_sm) *warps_per_sm = per_sm * dev::kWarpsPerBlock;
+  if (warps_per_sm) *warps_per_sm = per_sm * dev::warps_per_block<11>();
   if (sm_count) *sm_count = sms;
   return RECOIL_OK;
 }
+
+#ifdef RECOIL_TIMELINE
+extern "C" int recoil_timeline_read(unsigned long long *host, uint32_t n_tasks) {
+  const uint32_t n = n_tasks < recoil::dev::kTimelineMax ? n_tasks : recoil::dev::kTimelineMax;
+  return cudaMemcpyFromSymbol(host, recoil::dev::g_timeline, 32ull * n) == cudaSuccess ? 0 : -1;
+}
+#endif

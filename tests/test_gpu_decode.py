@@ -360,3 +360,33 @@ def test_decoder_side_combine(target):
     assert dec.plan["n_tasks"] == R.recoil_inspect(R.recoil_combine_splits(c, target))["n_splits"]
     assert (dec.output().cpu().numpy() == sym).all()
     dec.close()
+
+
+@pytest.mark.timeout(900)
+def test_beyond_2pow31_symbols():
+    """N > 2^31 symbols (config 5's 8 GiB stream is sharded into such spans): 64-bit symbol
+    indices through the fused task expansion (sync starts of groups >= 2^26), the whole stream
+    in one launch, the last two shards alone, the CPU decoder, and oracle-decoded sampled tasks."""
+    N = (1 << 31) + (1 << 21) + 777
+    sym = synth.image_bytes(N, synth.seed_for(5, 31))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 4096)
+    M = R.recoil_inspect(c)["n_splits"]
+    assert M == 4096
+    rc, bad, out, _ = gpu_decode(c)
+    assert rc == 0, (R.ERRORS.get(rc), bad)
+    mism = np.nonzero(out != sym)[0]
+    assert mism.size == 0, f"{mism.size} mismatches, first at {mism[:5]}"
+    del out
+    bounds = R.recoil_shard_plan(c, 8)
+    for tb, te in ((bounds[7], bounds[8]), (M - 3, M)):  # the last shard; three tasks wholly above 2^31
+        rc, bad, out, plan = gpu_decode(c, tb, te)
+        assert rc == 0, (R.ERRORS.get(rc), bad)
+        lo, hi = plan["out_lo"], plan["out_hi"]
+        assert hi == N and (te - tb > 3 or lo > (1 << 31))
+        assert (out == sym[lo:hi]).all()
+    full = np.zeros(N, dtype=np.uint8)
+    for t in (M // 2, M - 3, M - 2, M - 1):
+        want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t), full)
+        assert (want[lo:hi + 1] == sym[lo:hi + 1]).all(), t
+    assert (R.recoil_decode_cpu(c) == sym).all()
