@@ -47,8 +47,9 @@ seen = set()
 for i in np.argsort(st):
     if gw[i] not in seen:
         seen.add(gw[i]); first[i] = True
-blk, wib = gw // 8, gw % 8
-print("mean first-task duration by warp-in-block:", " ".join(f"{dur[first & (wib == k)].mean():6.1f}" for k in range(8)))
+wpb = int(os.environ.get("WPB", "24"))  # warps per block of the build
+blk, wib = gw // wpb, gw % wpb
+print("mean first-task duration by warp-in-block:", " ".join(f"{dur[first & (wib == k)].mean():6.1f}" for k in range(wpb)))
 rank = np.zeros(len(gw), int)
 for s in np.unique(sm):
     bl = np.unique(blk[sm == s])
@@ -56,3 +57,14 @@ for s in np.unique(sm):
         rank[(sm == s) & (blk == b)] = r
 print("mean first-task duration by block rank on its SM:", " ".join(f"{dur[first & (rank == k)].mean():6.1f}" for k in range(rank.max() + 1)))
 print("mean first-task duration by SMSP (warp-in-block % 4):", " ".join(f"{dur[first & (wib % 4 == k)].mean():6.1f}" for k in range(4)))
+b2 = blk
+rows = {}
+for i in range(len(gw)):
+    rows.setdefault(int(b2[i]), int(sm[i]))
+bl = sorted(rows)
+print("block -> SM (first 12):", [(b, rows[b]) for b in bl[:12]])
+print("block -> SM (148..159):", [(b, rows[b]) for b in bl[148:160]])
+persm = {}
+for b in bl:
+    persm.setdefault(rows[b], []).append(b)
+print("SM -> blocks (first 6 SMs):", [(s, persm[s]) for s in sorted(persm)[:6]])
