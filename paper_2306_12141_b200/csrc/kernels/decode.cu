@@ -50,10 +50,17 @@ namespace dev {
 #define RECOIL_WARPS 24
 #endif
 #ifndef RECOIL_WARPS_ADAPTIVE
-#define RECOIL_WARPS_ADAPTIVE 8
+#define RECOIL_WARPS_ADAPTIVE 32
 #endif
+// NB = 0 and NB = -1 are the adaptive codec (NEXT rows 1 + 4: index-keyed
+// models, 16-bit symbols, n at run time; model tables in dynamic shared memory):
+// one CTA of 32 warps per SM (2^25 latent symbols: 194 G symbols/s, against 184
+// at 2 x 16 warps and 165 at 3 x 8), or, when the tables leave no room for that
+// layout, 8-warp CTAs (NB = -1).
 template <int NB>
-__host__ __device__ constexpr int warps_per_block() { return NB == 0 ? RECOIL_WARPS_ADAPTIVE : RECOIL_WARPS; }
+__host__ __device__ constexpr int warps_per_block() {
+  return NB == 0 ? RECOIL_WARPS_ADAPTIVE : NB < 0 ? 8 : RECOIL_WARPS;
+}
 template <int NB>
 __host__ __device__ constexpr int threads_per_block() { return 32 * warps_per_block<NB>(); }
 // Resident warps per SM the register budget is sized for.  The steady state is
@@ -64,16 +71,14 @@ __host__ __device__ constexpr int threads_per_block() { return 32 * warps_per_bl
 #ifndef RECOIL_MIN_WARPS
 #define RECOIL_MIN_WARPS 48
 #endif
-// NB = 0 is the adaptive codec (NEXT rows 1 + 4: index-keyed models, 16-bit
-// symbols, n at run time); its model tables live in dynamic shared memory.
 template <int NB>
 __host__ __device__ constexpr int min_blocks() {
   constexpr int w = warps_per_block<NB>();
-  return NB == 0 ? (32 / w > 0 ? 32 / w : 1) : NB <= 12 ? (RECOIL_MIN_WARPS / w > 0 ? RECOIL_MIN_WARPS / w : 1)
+  return NB <= 0 ? (32 / w > 0 ? 32 / w : 1) : NB <= 12 ? (RECOIL_MIN_WARPS / w > 0 ? RECOIL_MIN_WARPS / w : 1)
                                                        : (40 / w > 0 ? 40 / w : 1);
 }
 template <int NB>
-__host__ __device__ constexpr int sym_bytes() { return NB == 0 ? 2 : 1; }
+__host__ __device__ constexpr int sym_bytes() { return NB <= 0 ? 2 : 1; }
 constexpr int kRingChunks = 4;
 constexpr int kRingWords = kRingChunks * (int)kChunkWords;  // 1024 words = 2 KB per warp
 constexpr uint32_t kRingBytes = 2 * kRingWords;
@@ -108,11 +113,13 @@ struct Params {
 constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 template <int NB>
 __host__ __device__ constexpr int lut_words() {
-  return NB == 0 ? 128 * warps_per_block<0>() : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512;
+  return NB <= 0 ? 128 * warps_per_block<NB>() : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512;
 }
 // bytes before the LUT: staging + records, padded to 7 KB mod 8 KB (see Smem)
 constexpr int kPreLut(int W, int S) { return W * ((int)kBlockBytes * S + 2 * (int)sizeof(TaskRec)); }
-constexpr int kLutPad(int W, int S) { return ((7168 - kPreLut(W, S) % 8192) % 8192 + 8192) % 8192; }
+// padding that puts the LUT at 1 KB + pre + pad = 0 mod A (A = 8 KB for the LOP3-addressed
+// LUT of n <= 11, else 2 KB so the rings after the LUT stay 2 KB-aligned)
+constexpr int kLutPad(int W, int S, int A) { return ((A - 1024 - kPreLut(W, S) % A) % A + A) % A; }
 // Block layout (byte offsets into the dynamic shared memory).  Order matters: the
 // CTA's shared memory starts 1 KB into its shared window (the reserved system
 // area), so stage + rec + pad (7 KB mod 8 KB) put the LUT on an 8 KB boundary,
@@ -132,7 +139,7 @@ struct Smem {
   static constexpr int W = warps_per_block<NB>();
   static constexpr int kStage = 0;
   static constexpr int kRec = kStage + W * (int)kBlockBytes * S;
-  static constexpr int kLut = kRec + W * 2 * (int)sizeof(TaskRec) + kLutPad(W, S);
+  static constexpr int kLut = kRec + W * 2 * (int)sizeof(TaskRec) + kLutPad(W, S, NB >= 1 && NB <= 11 ? 8192 : 2048);
   static constexpr int kRing = kLut + 4 * lut_words<NB>();
   static constexpr int kBytes = kRing + W * 2 * kRingWords;
 };
@@ -272,7 +279,7 @@ struct Warp {
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
   template <int NB>
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
-    if constexpr (NB == 0) {
+    if constexpr (NB <= 0) {
       // Eq. 2 under model mid(i) (P:227 item (3)): the entry j of the model
       // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (64 buckets of
       // the slot range per model) and a warp-converged binary search inside
@@ -383,8 +390,10 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
 
 template <int NB, bool FUSED>
 __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) recoil_decode_kernel(const Params p) {
-  constexpr int kWarpsPerBlock = warps_per_block<NB>();
-  constexpr int kThreads = threads_per_block<NB>();
+  // the shared-memory layout is sized for warps_per_block<NB>() warps; a launch
+  // may use fewer (small task counts are spread over all SMs, see launch())
+  const uint32_t kWarpsPerBlock = blockDim.x >> 5;
+  const uint32_t kThreads = blockDim.x;
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   using L = Smem<NB>;
   uint32_t *const sm_lut = reinterpret_cast<uint32_t *>(smem_dyn + L::kLut);
@@ -403,7 +412,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     hw_first = t0 < p.n_tasks ? __ldg(reinterpret_cast<const uint32_t *>(&p.heads[t0]) + (threadIdx.x & 7)) : 0u;
   }
   // a2: stage the LUT in shared memory (per block)
-  if constexpr (NB == 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
+  if constexpr (NB <= 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
     const uint32_t words = (p.ad_K * 66 * 2 + 15) / 16 * 4 + ((p.ad_E + 3) & ~3u) + p.ad_K;
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
@@ -420,7 +429,8 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   } else {
     for (uint32_t i = threadIdx.x; i < (1u << NB) / 16; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
-    if (threadIdx.x < 256) sm_lut[threadIdx.x] = reinterpret_cast<const uint32_t *>(p.lut + (1u << NB))[threadIdx.x];
+    for (uint32_t i = threadIdx.x; i < 256; i += kThreads)
+      sm_lut[i] = reinterpret_cast<const uint32_t *>(p.lut + (1u << NB))[i];
   }
   __syncthreads();
 
@@ -433,7 +443,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
   w.gt = lanemask_gt();
   w.lut32 = smem_addr(sm_lut);
-  if constexpr (NB == 0) {
+  if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
     w.ent32 = w.coarse32 + (p.ad_K * 66 * 2 + 15) / 16 * 16;
@@ -622,7 +632,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       return make_uint4(v[0], v[1], v[2], v[3]);
     };
     auto stage_block = [&](int blk) {
-      if constexpr (NB == 0) {
+      if constexpr (NB <= 0) {
         const uint4 v = (mid_blk == blk) ? midv : mid_load(blk);
         __syncwarp();
         sts_v4(w.mid32 - lane + 16 * lane, v);
@@ -722,8 +732,8 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
 }
 
 using KernelFn = void (*)(const Params);
-static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false) {
-  if (adaptive) return fused ? recoil_decode_kernel<0, true> : nullptr;
+static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false, bool narrow = false) {
+  if (adaptive) return !fused ? nullptr : narrow ? recoil_decode_kernel<-1, true> : recoil_decode_kernel<0, true>;
   if (fused) switch (nbits) {
     case 1: return recoil_decode_kernel<1, true>;
     case 2: return recoil_decode_kernel<2, true>;
@@ -766,8 +776,9 @@ static KernelFn kernel_for(uint32_t nbits, bool fused, bool adaptive = false) {
 
 }  // namespace dev
 
-static size_t layout_bytes(uint32_t nbits) {  // dev::Smem<n>::kBytes (n = 0: adaptive)
+static size_t layout_bytes(int nbits) {  // dev::Smem<n>::kBytes (n = 0 / -1: adaptive)
   switch (nbits) {
+    case -1: return dev::Smem<-1>::kBytes;
     case 0: return dev::Smem<0>::kBytes;
     case 10: return dev::Smem<10>::kBytes;
     case 11: return dev::Smem<11>::kBytes;
@@ -779,7 +790,7 @@ static size_t smem_bytes(uint32_t nbits) {  // the block layout + the slot -> sy
   return layout_bytes(nbits) + (nbits > (uint32_t)dev::kNarrowMaxBits ? (size_t)1 << nbits : 0);
 }
 static size_t dyn_smem(const Decoder &d) {  // adaptive: the layout + the model tables
-  return d.c->adaptive ? layout_bytes(0) + d.lut.size() : smem_bytes(d.plan.prob_bits);
+  return d.c->adaptive ? layout_bytes(d.ad_narrow ? -1 : 0) + d.lut.size() : smem_bytes(d.plan.prob_bits);
 }
 
 // The kernel's dynamic shared-memory limit only ever grows (per device and
@@ -793,8 +804,11 @@ static int ensure_dyn(dev::KernelFn fn, size_t dyn) {
   };
   static std::mutex mu;
   static std::vector<Lim> lims;
-  int dev_id = 0;
-  if (cudaGetDevice(&dev_id) != cudaSuccess) return RECOIL_E_CUDA;
+  int dev_id = 0, optin = 0;
+  if (cudaGetDevice(&dev_id) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (dyn > (size_t)optin) return RECOIL_E_UNSUPPORTED;  // tables do not fit in shared memory
   std::lock_guard<std::mutex> lock(mu);
   for (Lim &l : lims)
     if (l.dev == dev_id && l.fn == fn) {
@@ -821,12 +835,30 @@ static int occupancy(dev::KernelFn fn, int threads, size_t dyn, int *blocks_per_
   return RECOIL_OK;
 }
 
+// Adaptive kernels: 32-warp CTAs (NB = 0) when their layout plus the model tables
+// fit the opt-in shared memory of one block, else 8-warp CTAs (NB = -1).
+static int adaptive_narrow(size_t table_bytes, int *narrow) {
+  int dev_id = 0, optin = 0;
+  if (cudaGetDevice(&dev_id) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  *narrow = layout_bytes(0) + table_bytes > (size_t)optin;
+  return RECOIL_OK;
+}
+
 static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *d_mid, uint8_t *d_out,
                   cudaStream_t s) {
   const recoil_plan &pl = d->plan;
   const bool adaptive = d->c->adaptive;
-  dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive);
-  const int warps = adaptive ? dev::warps_per_block<0>() : dev::warps_per_block<11>();
+  if (adaptive && d->blocks_per_sm == 0) {  // 32-warp CTAs unless the model tables leave no room
+    int narrow = 0;
+    int rc = adaptive_narrow(d->lut.size(), &narrow);
+    if (rc) return rc;
+    d->ad_narrow = narrow != 0;
+  }
+  dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive, d->ad_narrow);
+  const int warps = adaptive ? (d->ad_narrow ? dev::warps_per_block<-1>() : dev::warps_per_block<0>())
+                             : dev::warps_per_block<11>();
   if (d->blocks_per_sm == 0) {
     // launch geometry, cached per (device, kernel, dynamic smem) for the process: the
     // attribute / occupancy queries cost tens of microseconds, and the pipeline builds a
@@ -878,13 +910,19 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.ad_K = d->ad_K;
   prm.ad_E = d->ad_E;
   prm.nbits = pl.prob_bits;
-  const uint32_t need = (pl.n_tasks + warps - 1) / warps;
+  // fewer tasks than resident warps: narrower blocks, so the tasks spread over
+  // all SMs instead of filling a few (config 4 at 2048 splits: 86 SMs x 24 warps)
+  const uint32_t cap = (uint32_t)(d->blocks_per_sm * d->sm_count) * (uint32_t)warps;
+  const uint32_t wl = pl.n_tasks >= cap ? (uint32_t)warps
+                                        : std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)warps,
+                                              (pl.n_tasks + d->sm_count - 1) / (uint32_t)d->sm_count));
+  const uint32_t need = (pl.n_tasks + wl - 1) / wl;
   const uint32_t grid = std::min<uint32_t>(need, (uint32_t)(d->blocks_per_sm * d->sm_count));
   if (d->c->adaptive) {  // container-sized tables: the limit may have to grow
     int rc = ensure_dyn(fn, dyn_smem(*d));
     if (rc) return rc;
   }
-  fn<<<grid, 32 * warps, dyn_smem(*d), s>>>(prm);
+  fn<<<grid, 32 * wl, dyn_smem(*d), s>>>(prm);
   return cudaGetLastError() == cudaSuccess ? RECOIL_OK : RECOIL_E_CUDA;
 }
 
@@ -986,13 +1024,19 @@ extern "C" int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes
   int prev = 0;
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
-  int per_sm = 0, sms = 0;
-  int rc = occupancy(dev::kernel_for(16, true, true), dev::threads_per_block<0>(), layout_bytes(0) + (size_t)table_bytes, &per_sm);
+  int per_sm = 0, sms = 0, narrow = 0;
+  int rc = adaptive_narrow((size_t)table_bytes, &narrow);
+  const int warps = narrow ? dev::warps_per_block<-1>() : dev::warps_per_block<0>();
+  if (!rc)
+    rc = narrow ? occupancy(dev::kernel_for(16, true, true, true), dev::threads_per_block<-1>(),
+                            layout_bytes(-1) + (size_t)table_bytes, &per_sm)
+                : occupancy(dev::kernel_for(16, true, true, false), dev::threads_per_block<0>(),
+                            layout_bytes(0) + (size_t)table_bytes, &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;
   if (e2 != cudaSuccess) return RECOIL_E_CUDA;
-  if (warps_per_sm) *warps_per_sm = per_sm * dev::warps_per_block<0>();
+  if (warps_per_sm) *warps_per_sm = per_sm * warps;
   if (sm_count) *sm_count = sms;
   return RECOIL_OK;
 }

@@ -113,6 +113,7 @@ struct Decoder {
   int single_symbol = -1;          // >= 0: the model has one symbol (f = 2^n): decode = fill
   uint32_t ad_K = 0, ad_E = 0;     // adaptive: models, table entries (lut = coarse | entries | offsets)
   int blocks_per_sm = 0, sm_count = 0;  // launch geometry (occupancy API), cached
+  bool ad_narrow = false;          // adaptive: 8-warp CTAs (the model tables leave no room for 32 warps)
 };
 
 int build_decoder(const uint8_t *c, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,

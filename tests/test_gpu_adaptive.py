@@ -141,3 +141,24 @@ def test_wrong_model_ids_and_static_entry_point():
         R.recoil_decode(dec.handle, dec.workspace.data_ptr(), dec.words.data_ptr(), dec.out.data_ptr(),
                         dec.stream_handle)
     dec.close()
+
+
+@pytest.mark.parametrize("K,length", [(4, 7000), (2, 20000)])
+def test_large_model_tables_use_narrow_ctas(K, length):
+    """Model tables too large for the 32-warp CTA layout (~100 KB of tables) run on the 8-warp
+    adaptive kernel; the occupancy query reports the same geometry; output bit-exact."""
+    rng = np.random.default_rng(K * length)
+    base, ln, fs = [], [], []
+    for k in range(K):
+        hist = rng.integers(1, 1000, size=length).astype(np.uint64)
+        base.append(k * length)
+        ln.append(length)
+        fs.append(oracle.quantize(hist, 16))
+    models = {"base": np.array(base, np.uint32), "len": np.array(ln, np.uint32), "f": np.concatenate(fs)}
+    table_bytes = (K * 132 + 15) // 16 * 16 + 4 * (((K * length + 3) & ~3) + K)
+    assert table_bytes > 105_000  # the 32-warp layout (125 KB) leaves ~102 KB of the 227 KB
+    warps, _ = R.recoil_decode_occupancy_adaptive(0, table_bytes)
+    assert warps >= 8 and warps % 8 == 0
+    sym, mid = _draw(rng, models, 300_000, K)
+    c = R.recoil_encode_adaptive(sym, mid, models, 16, 64)
+    _check(c, mid, sym, oracle_check=True)
