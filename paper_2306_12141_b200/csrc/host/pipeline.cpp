@@ -159,7 +159,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       char *ws = set;
       uint16_t *words = reinterpret_cast<uint16_t *>(set + pl->ws_bytes);
       uint8_t *dout = reinterpret_cast<uint8_t *>(set + pl->ws_bytes + pl->word_bytes);
-      // stage LUT + finals + tasks in pinned memory once the set's previous H2D has consumed it
+      // stage LUT + finals + tasks (+ records) in pinned memory once the set's previous H2D has consumed it
       if (k >= n_streams && cudaEventSynchronize(pl->staged[s]) != cudaSuccess) return RECOIL_E_CUDA;
       uint8_t *stg = pl->staging[s];
       std::memset(stg, 0, 16);
@@ -167,16 +167,13 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (!d.finals.empty()) std::memcpy(stg + d.finals_off, d.finals.data(), 4 * d.finals.size());
       if (!d.tasks.empty()) std::memcpy(stg + d.tasks_off, d.tasks.data(), sizeof(TaskRec) * d.tasks.size());
       if (!d.heads.empty()) std::memcpy(stg + d.tasks_off, d.heads.data(), sizeof(TaskHead) * d.heads.size());
-      const uint64_t staged_bytes = d.fused ? d.rec_off : pn.workspace_bytes;  // raw records: from the container
+      if (d.fused) {  // the raw split records and the zero pad under their windows: one H2D with the tables
+        if (d.rec_len) std::memcpy(stg + d.rec_off, c->bytes + d.rec_src, d.rec_len);
+        std::memset(stg + d.rec_off + d.rec_len, 0, pn.workspace_bytes - d.rec_off - d.rec_len);
+      }
       if (k >= n_streams && cudaStreamWaitEvent(sh, pl->ev_out[s], 0) != cudaSuccess) return RECOIL_E_CUDA;
-      if (cudaMemcpyAsync(ws, stg, staged_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      if (cudaMemcpyAsync(ws, stg, pn.workspace_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaEventRecord(pl->staged[s], st) != cudaSuccess)
-        return RECOIL_E_CUDA;
-      if (d.rec_len && cudaMemcpyAsync(ws + d.rec_off, c->bytes + d.rec_src, d.rec_len, cudaMemcpyHostToDevice,
-                                       st) != cudaSuccess)
-        return RECOIL_E_CUDA;
-      if (d.fused && cudaMemsetAsync(ws + d.rec_off + d.rec_len, 0, pn.workspace_bytes - d.rec_off - d.rec_len, st) !=
-                         cudaSuccess)  // pad under the record windows
         return RECOIL_E_CUDA;
       const uint64_t have = c->B > pn.word_lo ? std::min<uint64_t>(pn.word_count, c->B - pn.word_lo) : 0;
       if (have && cudaMemcpyAsync(words, c->words + 2 * pn.word_lo, 2 * have, cudaMemcpyHostToDevice, st) !=
@@ -187,7 +184,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
         return RECOIL_E_CUDA;
       if (cudaEventRecord(pl->ev_in[s], sh) != cudaSuccess || cudaStreamWaitEvent(sc, pl->ev_in[s], 0) != cudaSuccess)
         return RECOIL_E_CUDA;
-      rc = recoil_decode(reinterpret_cast<recoil_decoder *>(&d), ws, words, dout, sc);
+      rc = decode_staged(&d, ws, words, dout, sc);  // the status block came zeroed with the tables
       if (rc) return rc;
       if (cudaEventRecord(pl->ev_k[s], sc) != cudaSuccess || cudaStreamWaitEvent(so, pl->ev_k[s], 0) != cudaSuccess)
         return RECOIL_E_CUDA;

@@ -965,6 +965,24 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
   return RECOIL_OK;
 }
 
+namespace recoil {
+// recoil_decode without the status reset: the caller uploaded a zeroed status
+// block with the workspace on the same stream order (the e2e pipeline's one
+// H2D of tables + records per chunk)
+int decode_staged(Decoder *d, char *ws, const uint16_t *d_words, uint8_t *d_out, void *stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const recoil_plan &pl = d->plan;
+  if (pl.n_tasks == 0) return RECOIL_OK;
+  if (d->c->adaptive) return RECOIL_E_ARG;
+  if (d->single_symbol >= 0)
+    return cudaMemsetAsync(d_out + (pl.out_lo - pl.out_base), d->single_symbol, pl.out_hi - pl.out_lo, s) ==
+                   cudaSuccess
+               ? RECOIL_OK
+               : RECOIL_E_CUDA;
+  return launch(d, ws, d_words, nullptr, d_out, s);
+}
+}  // namespace recoil
+
 extern "C" int recoil_decode(recoil_decoder *dec, void *d_workspace, const uint16_t *d_words, uint8_t *d_out,
                              void *stream) {
   if (!dec || !d_workspace || !d_words) return RECOIL_E_ARG;

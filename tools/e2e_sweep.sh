@@ -3,7 +3,7 @@
 TAG=${1:-r}; export TAG
 cd "$(dirname "$0")/.." && mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-for cs in "4 2" "8 2" "8 3" "16 3" "16 4" "32 4"; do
+for cs in ${E2E_SWEEP:-"4 2" "8 2" "8 3" "16 3" "16 4" "32 4"}; do
   set -- $cs
   timeout 300 python bench.py --steps 10 --no-cpu --no-extra --chunks $1 --streams $2 2>/dev/null | tail -1 > gpurun_out/e2e_$TAG.json
   python - "$1" "$2" <<'PY'
