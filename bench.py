@@ -464,10 +464,20 @@ def main():
             d20.decode()
             ok20 = d20.status()[0] == 0 and bool((d20.output().cpu().numpy() == sym).all())
             t20 = timed_decode(d20, args.steps, args.warmup)
+            d20.close()
+            p20 = R.recoil_partitioned_encode(sym, f, 11, M20)  # the partitioned baseline at the same count
+            q20 = R.GpuDecoder(p20, local, stream=stream)
+            q20.upload()
+            q20.decode()
+            pok20 = q20.status()[0] == 0 and bool((q20.output().cpu().numpy() == sym).all())
+            tp20 = timed_decode(q20, args.steps, args.warmup)
+            q20.close()
             extra["config2_20k"] = {"value": round(N_total * args.steps / (sum(t20) / 1e3) / 1e9, 2), "unit": "GB/s",
                                     "splits": R.recoil_inspect(c20)["n_splits"], "bit_exact": ok20,
-                                    "ms_per_step": round(float(np.mean(t20)), 4)}
-            d20.close()
+                                    "ms_per_step": round(float(np.mean(t20)), 4),
+                                    "partitioned_baseline": {
+                                        "value": round(N_total * args.steps / (sum(tp20) / 1e3) / 1e9, 2),
+                                        "unit": "GB/s", "partitions": M20, "bit_exact": pok20}}
         if world == 1 and not args.no_adaptive:
             extra["adaptive_latent"] = adaptive_extra(args, local, stream, timed_decode, peak_hbm())
     cpu = None
