@@ -48,11 +48,14 @@ def main():
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
     for spec in sys.argv[2:]:
-        cfg, M = spec.split(":")
-        rep = os.path.join(ROOT, "gpurun_out", f"prof_{cfg}_{tag}.ncu-rep")
+        # "config3:14208", or "config4@2048:2048" for a capture named prof_config4_2048_<tag>
+        cfgv, M = spec.split(":")
+        cfg, _, var = cfgv.partition("@")
+        name = f"{cfg}_{var}" if var else cfg
+        rep = os.path.join(ROOT, "gpurun_out", f"prof_{name}_{tag}.ncu-rep")
         s = summary(rep)
         s["source"] = f"ncu --set full --clock-control none, 1 decode launch of bench.py --config {cfg} ({M} splits)"
-        dst = os.path.join(ROOT, "profiles", f"r01_decode_{cfg}_ncu_full.json")
+        dst = os.path.join(ROOT, "profiles", f"r01_decode_{name}_ncu_full.json")
         json.dump(s, open(dst, "w"), indent=1)
         rd = s["dram__bytes_read.sum"]["value"] * UNIT[s["dram__bytes_read.sum"]["unit"]]
         wr = s["dram__bytes_write.sum"]["value"] * UNIT[s["dram__bytes_write.sum"]["unit"]]
