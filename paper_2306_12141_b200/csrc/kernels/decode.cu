@@ -19,13 +19,15 @@
 // 16-group blocks (one 512-byte output block each) with no per-group branch.
 //
 // Memory path: the words come from a per-warp 2 KB shared-memory ring filled
-// by warp-cooperative 16-byte cp.async loads (256 words per chunk, two chunks
-// of look-ahead, checked every 8 groups since 8 groups consume <= 256 words);
-// task records stream in by cp.async one task ahead, tasks are handed out by
-// an atomic counter (persistent warps); decoded bytes are staged per output
-// block in shared memory and leave as one 16-byte store per lane (byte stores
-// only in the one 16-byte chunk per commit edge).  All shared accesses use
-// 32-bit shared-window addresses (inline PTX) computed once per warp.
+// by warp-cooperative 16-byte cp.async loads (256 words per chunk; chunks c,
+// c-1, c-2 resident and c-3 in flight, checked once per 16-group block since 16
+// groups consume <= 512 words); Recoil task heads and raw split records are
+// loaded one block before a task starts and expanded in the kernel (row a1),
+// prebuilt records (partitioned containers) stream in by cp.async; tasks are
+// handed out by an atomic counter (persistent warps, 2 CTAs of 24 warps per
+// SM); decoded bytes are staged per output block in shared memory and leave as
+// one 16-byte store per lane.  All shared accesses use 32-bit shared-window
+// addresses (inline PTX) computed once per warp.
 #include <cuda_runtime.h>
 
 #include <algorithm>
