@@ -180,6 +180,18 @@ int recoil_decoder_create(const uint8_t *container, uint64_t len, uint64_t task_
  * partitioned container. */
 int recoil_decoder_create_subset(const uint8_t *container, uint64_t len, uint32_t target_splits,
                                  uint64_t task_begin, uint64_t task_end, recoil_decoder **out);
+/* Decoder-side combine into tasks of unequal length (P:266-272 on the client:
+ * which split points a decoder uses is its choice).  Tasks in stream order:
+ * the first run_tasks[0] tasks each span run_splits[0] consecutive encoder
+ * splits, the next run_tasks[1] span run_splits[1], ...; the last task takes
+ * the splits that remain (fewer tasks if the splits run out).  The kernel's
+ * first wave takes tasks 0, 1, ... and later ones come from its atomic
+ * counter, so long tasks first and short ones last (longest-processing-time
+ * order) let the warps the SM schedulers favour take more of the tail.  Output
+ * identical to any other plan.  Errors as recoil_decoder_create_subset; E_ARG
+ * for n_runs = 0 or a run of 0 splits. */
+int recoil_decoder_create_grouped(const uint8_t *container, uint64_t len, uint32_t n_runs,
+                                  const uint32_t *run_tasks, const uint32_t *run_splits, recoil_decoder **out);
 int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan);
 
 /* Asynchronous host->device copy on cuda_stream of the packed LUT and task

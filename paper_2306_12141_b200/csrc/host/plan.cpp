@@ -389,6 +389,57 @@ extern "C" int recoil_decoder_create_subset(const uint8_t *container, uint64_t l
   }
 }
 
+extern "C" int recoil_decoder_create_grouped(const uint8_t *container, uint64_t len, uint32_t n_runs,
+                                             const uint32_t *run_tasks, const uint32_t *run_splits,
+                                             recoil_decoder **out) {
+  if (!container || !out || n_runs < 1 || !run_tasks || !run_splits) return RECOIL_E_ARG;
+  *out = nullptr;
+  try {
+    auto full = std::make_shared<Container>();
+    int rc = parse_container(container, len, full.get(), /*light=*/true);
+    if (rc) return rc;
+    if (full->partitioned) return RECOIL_E_ARG;  // partitions cannot be combined
+    for (uint32_t r = 0; r < n_runs; ++r)
+      if (run_splits[r] == 0) return RECOIL_E_ARG;
+    // task i spans run_splits[r] consecutive encoder splits (segments) for the
+    // run r it falls in; the point after its last segment is kept, every other
+    // point is dropped (the decode runs through it); the last task
+    // takes the segments that remain
+    auto view = std::make_shared<Container>(*full);
+    const uint64_t P = full->M - 1;
+    view->offset.clear();
+    view->maxg.clear();
+    view->rec_off.clear();
+    uint64_t seg = 0, last = 0;
+    bool any = false;
+    for (uint32_t r = 0; r < n_runs; ++r)
+      for (uint32_t i = 0; i < run_tasks[r]; ++i) {
+        seg += run_splits[r];
+        if (seg > P) break;
+        const uint64_t k = seg - 1;  // point k closes segment k
+        view->offset.push_back(full->offset[k]);
+        view->maxg.push_back(full->maxg[k]);
+        view->rec_off.push_back(full->rec_off[k]);
+        last = k;
+        any = true;
+      }
+    view->M = (uint32_t)view->offset.size() + 1;
+    // rec_off[j + 1] bounds kept record j's bytes (the next kept record: a looser
+    // but valid bound); the last bound is the last kept record's end
+    view->rec_off.push_back(any ? full->rec_off[last + 1] : full->rec_off[0]);
+    Decoder *d = new Decoder();
+    rc = build_decoder_from(view, 0, UINT64_MAX, d, true);
+    if (rc) {
+      delete d;
+      return rc;
+    }
+    *out = reinterpret_cast<recoil_decoder *>(d);
+    return RECOIL_OK;
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}
+
 extern "C" int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan) {
   if (!dec || !plan) return RECOIL_E_ARG;
   *plan = reinterpret_cast<const Decoder *>(dec)->plan;

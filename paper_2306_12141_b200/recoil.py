@@ -35,6 +35,7 @@ EXPORTS = [
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
     "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
     "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive", "recoil_decoder_create_subset",
+    "recoil_decoder_create_grouped",
 ]
 
 
@@ -106,6 +107,7 @@ def load(path: str = LIB_PATH):
         "recoil_decode_adaptive": (i32, [P, P, P, P, P, P]),
         "recoil_decode_occupancy_adaptive": (i32, [i32, u64, P, P]),
         "recoil_decoder_create_subset": (i32, [P, u64, u32, u64, u64, P]),
+        "recoil_decoder_create_grouped": (i32, [P, u64, u32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -241,6 +243,20 @@ def recoil_decoder_create_subset(container, target_splits: int, task_begin: int 
     return h
 
 
+def recoil_decoder_create_grouped(container, run_tasks, run_splits) -> ctypes.c_void_p:
+    """Tasks in stream order: run_tasks[r] tasks of run_splits[r] encoder splits each, the last task
+    takes the rest."""
+    c = _u8(container)
+    rt = np.ascontiguousarray(np.asarray(run_tasks, dtype=np.uint32))
+    rs = np.ascontiguousarray(np.asarray(run_splits, dtype=np.uint32))
+    if rt.size != rs.size:
+        raise ValueError("run_tasks and run_splits differ in length")
+    h = ctypes.c_void_p()
+    _check(load().recoil_decoder_create_grouped(c.ctypes.data, c.size, rt.size, _ptr(rt), _ptr(rs),
+                                                ctypes.byref(h)), "recoil_decoder_create_grouped")
+    return h
+
+
 def recoil_decoder_plan(handle) -> dict:
     p = recoil_plan()
     _check(load().recoil_decoder_plan(handle, ctypes.byref(p)), "recoil_decoder_plan")
@@ -307,12 +323,15 @@ class GpuDecoder:
     """
 
     def __init__(self, container, device: int = 0, task_begin: int = 0, task_end: int = (1 << 64) - 1,
-                 stream=None, subset: int | None = None):
+                 stream=None, subset: int | None = None, grouped=None):
         import torch
         self.container = _u8(container)
         self.device = torch.device("cuda", device)
-        self.handle = (recoil_decoder_create(self.container, task_begin, task_end) if subset is None else
-                       recoil_decoder_create_subset(self.container, subset, task_begin, task_end))
+        if grouped is not None:  # (run_tasks, run_splits): recoil_decoder_create_grouped
+            self.handle = recoil_decoder_create_grouped(self.container, *grouped)
+        else:
+            self.handle = (recoil_decoder_create(self.container, task_begin, task_end) if subset is None else
+                           recoil_decoder_create_subset(self.container, subset, task_begin, task_end))
         self.plan = recoil_decoder_plan(self.handle)
         p = self.plan
         self.stream = stream or torch.cuda.current_stream(self.device)

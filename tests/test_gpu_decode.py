@@ -259,11 +259,11 @@ def test_config4_combine_65536_to_2048_256_16():
 
 def test_config5_1GiB_image_residual_bench_launch():
     """Config 5 per GPU (1 GiB image-residual bytes) with the bench's split rule
-    (2 waves of resident warps), in one launch; sampled tasks against the oracle."""
+    (1.5 waves of resident warps), in one launch; sampled tasks against the oracle."""
     warps, sms = R.recoil_decode_occupancy(0, 11)
     sym = synth.image_bytes(1 << 30, synth.seed_for(5))
     f = R.recoil_build_model(synth.histogram(sym), 11)
-    c = R.recoil_encode(sym, f, 11, warps * sms * 2)
+    c = R.recoil_encode(sym, f, 11, warps * sms * 3 // 2)
     rc, bad, out, _ = gpu_decode(c)
     assert rc == 0 and (out == sym).all()
     _sampled_oracle_tasks(c, out, 8)

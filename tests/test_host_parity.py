@@ -345,3 +345,31 @@ def test_decoder_side_combine_plans_equal_combined_containers():
         assert all(p[k] == p2[k] for k in keys), target
     with pytest.raises(R.RecoilError):
         R.recoil_decoder_create_subset(R.recoil_partitioned_encode(sym, f, 11, 8), 2)
+
+
+def test_grouped_plans():
+    """recoil_decoder_create_grouped: uniform runs of k splits plan exactly what the combine rule
+    (points k, 2k, ...) plans; mixed runs give the requested task count; bad runs fail."""
+    sym = synth.exp_bytes(2_000_000, 50, 3)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 1000)
+    M = R.recoil_inspect(c)["n_splits"]
+    keys = ("n_tasks", "word_lo", "word_count", "out_lo", "out_hi", "out_base", "out_count")
+    for k in (1, 2, 3, 7, 999, 1000, 5000):
+        h = R.recoil_decoder_create_grouped(c, [M], [k])
+        p = R.recoil_decoder_plan(h)
+        R.recoil_decoder_destroy(h)
+        h2 = R.recoil_decoder_create_subset(c, -(-M // k))
+        p2 = R.recoil_decoder_plan(h2)
+        R.recoil_decoder_destroy(h2)
+        assert all(p[key] == p2[key] for key in keys), k
+    # long tasks first, short ones last: 300 tasks of 2 splits, then single splits
+    h = R.recoil_decoder_create_grouped(c, [300, M], [2, 1])
+    p = R.recoil_decoder_plan(h)
+    R.recoil_decoder_destroy(h)
+    assert p["n_tasks"] == 300 + (M - 600) and (p["out_lo"], p["out_hi"]) == (0, len(sym))
+    for bad in (([], []), ([5], [0])):
+        with pytest.raises((R.RecoilError, ValueError)):
+            R.recoil_decoder_create_grouped(c, *bad)
+    with pytest.raises(R.RecoilError):
+        R.recoil_decoder_create_grouped(R.recoil_partitioned_encode(sym, f, 11, 8), [2], [2])
