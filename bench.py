@@ -222,7 +222,7 @@ def run_reference(args, rank, world):
     # x SMs per GPU; the SM count is read from torch, not from our library
     import torch
     sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
-    waves = args.waves or 1.5
+    waves = args.waves or (1 if args.config == "config2" else 1.5)
     M = args.splits or (16 if args.config == "config1" else int(round(48 * sms * waves))) * world
     c = R.recoil_encode(sym, f, 11, M)
     M = R.recoil_inspect(c)["n_splits"]
@@ -259,9 +259,10 @@ def main():
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: time the optional NCCL gather of the ranks' spans to rank 0 (outside the decode)")
     ap.add_argument("--waves", type=float, default=0,
-                    help="splits per GPU = waves x resident warps; 0 = 1.5: the kernel runs 2 CTAs per SM and the "
-                         "SM schedulers favour the first, whose warps then take the last half wave (DESIGN.md §13; "
-                         "measured best against 1, 1.25, 2, 3 waves on configs 2, 3 and 5)")
+                    help="splits per GPU = waves x resident warps; 0 = per-config default: configs 3/5 1.5 (the "
+                         "kernel runs 2 CTAs per SM and the SM schedulers favour the first, whose warps then take the "
+                         "last half wave; DESIGN.md §13), config 2 1 (one split per resident warp: equal GB/s, and "
+                         "the closest to the partitioned baseline at the same count)")
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
     ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
     ap.add_argument("--chunks", type=int, default=8, help="e2e pipeline chunks per GPU")
@@ -303,7 +304,7 @@ def main():
     f = R.recoil_build_model(hist, 11)
     warps, sms = R.recoil_decode_occupancy(local, 11)
     if not args.waves:
-        args.waves = 1.5
+        args.waves = 1 if args.config == "config2" else 1.5
     M_gpu = args.splits or (16 if args.config == "config1" else int(round(warps * sms * args.waves)))
     if args.config == "config4":
         c_full = R.recoil_encode(sym, f, 11, 65536 * world)
