@@ -241,7 +241,11 @@ struct Warp {
   uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax;
   uint32_t gt;       // lanes above this one
   int lane;
-  int cursor2;       // 2 x (slice-relative index of the next word to read)
+  // 2 x (slice-relative index of the next word to read), unsigned: slices hold
+  // < 2^31 words, so the doubled index needs all 32 bits (a signed form
+  // overflowed for slices of >= 2^30 words: the 8 GiB config 5 stream in one
+  // launch); the only negative cursor of a valid stream is the end state -1
+  uint32_t cursor2;
   int cchunk;        // cursor2 >> 9 at the last window check
 
   // a7: warp-cooperative prefetch of word chunk c (256 words = 32 lanes x 16 B)
@@ -255,7 +259,7 @@ struct Warp {
   // 4-chunk ring).  16 groups consume at most 512 words (two chunks), so one
   // check covers a whole output block.
   __device__ __forceinline__ void window_check() {
-    const int c = cursor2 >> 9;
+    const int c = (int)(cursor2 >> 9);
     if (c != cchunk) {
       __syncwarp();  // all lanes' reads of the slot being refilled (chunk c+1's) are done
       do {
@@ -274,8 +278,8 @@ struct Warp {
     const uint32_t m = __ballot_sync(kFull, need);
     const int pre = __popc(m & gt);
     const int step2 = __reduce_add_sync(kFull, need ? -2 : 0);  // -2 x (words this group)
-    const uint32_t w = lds_u16(ring32 | ((uint32_t)(cursor2 + pre * p->neg2) & (kRingBytes - 2)));
-    cursor2 += step2;
+    const uint32_t w = lds_u16(ring32 | ((cursor2 + (uint32_t)(pre * p->neg2)) & (kRingBytes - 2)));
+    cursor2 += (uint32_t)step2;
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   }
   // a7: the task's word window: chunks c, c-1, c-2 resident, c-3 in flight
   auto issue_window = [&](int32_t cursor0) {
-    w.cursor2 = 2 * cursor0;
+    w.cursor2 = 2u * (uint32_t)cursor0;
     w.cchunk = cursor0 >> 8;
     w.issue_chunk(w.cchunk);
     w.issue_chunk(w.cchunk - 1);
@@ -708,9 +712,12 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     // a9: integrity -- a task that reaches its codec's start must end in the
     // stack-property end state: cursor one below the codec's first word,
     // every initialised lane back at L.
-    const int cursor = w.cursor2 >> 1;
+    // the cursor as a signed slice index: -1 is the codec's end state; anything
+    // else at or beyond the slice end is an underflow (the slice has < 2^31 words)
+    const uint32_t cur_u = w.cursor2 >> 1;
+    const int cursor = w.cursor2 == 0xFFFFFFFEu ? -1 : (int)cur_u;
     bool bad_end = false;
-    const bool under = cursor < -1;
+    const bool under = w.cursor2 != 0xFFFFFFFEu && cur_u >= (uint32_t)p.n_chunks * kChunkWords;
     if (end_cursor != kNoEndCheck) {
       const bool lane_ok = (init_group < lo_group) || x == kL;
       bad_end = (cursor != (int)end_cursor) || !__all_sync(kFull, lane_ok);

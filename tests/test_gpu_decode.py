@@ -390,3 +390,38 @@ def test_beyond_2pow31_symbols():
         want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t), full)
         assert (want[lo:hi + 1] == sym[lo:hi + 1]).all(), t
     assert (R.recoil_decode_cpu(c) == sym).all()
+
+
+@pytest.mark.timeout(1800)
+def test_config5_8GiB_full_size_sharded():
+    """BASELINE config 5 at its full size: one 8 GiB image-residual stream with the bench's
+    8-GPU split count (8 x 1.5 waves of resident warps), decoded in one launch and as the 8
+    split-range shards the 8-rank run uses (one after another on this GPU); every byte against
+    the input, sampled tasks against the oracle."""
+    warps, sms = R.recoil_decode_occupancy(0, 11)
+    N = 8 << 30
+    sym = synth.image_bytes(N, synth.seed_for(5))
+    hist = np.zeros(256, np.uint64)
+    for i in range(0, N, 1 << 28):
+        hist += np.bincount(sym[i:i + (1 << 28)], minlength=256).astype(np.uint64)
+    f = R.recoil_build_model(hist, 11)
+    M = 8 * (warps * sms * 3 // 2)
+    c = R.recoil_encode(sym, f, 11, M)
+    assert R.recoil_inspect(c)["n_splits"] == M
+    rc, bad, out, _ = gpu_decode(c)
+    assert rc == 0, (R.ERRORS.get(rc), bad)
+    assert out.size == N and np.array_equal(out, sym)
+    del out
+    bounds = R.recoil_shard_plan(c, 8)
+    covered = 0
+    for a, b in zip(bounds, bounds[1:]):
+        rc, bad, out, plan = gpu_decode(c, a, b)
+        assert rc == 0, (R.ERRORS.get(rc), bad)
+        assert plan["out_lo"] == covered and np.array_equal(out, sym[plan["out_lo"]:plan["out_hi"]])
+        covered = plan["out_hi"]
+        del out
+    assert covered == N
+    full = np.zeros(N, dtype=np.uint8)
+    for t in (0, M // 3, M - 2, M - 1):
+        want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t), full)
+        assert np.array_equal(want[lo:hi + 1], sym[lo:hi + 1]), t
