@@ -421,6 +421,15 @@ def test_config5_8GiB_full_size_sharded():
         covered = plan["out_hi"]
         del out
     assert covered == N
+    # end to end through the public host API: pinned container -> pinned symbols
+    pinned = torch.empty(len(c), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = c
+    hout = torch.zeros(N, dtype=torch.uint8, pin_memory=True)
+    pipe = R.HostPipeline(pinned.numpy(), 0, n_chunks=8, n_streams=3)
+    pipe.run(hout)
+    assert pipe.status()[0] == 0 and np.array_equal(hout.numpy(), sym)
+    pipe.close()
+    del hout, pinned
     full = np.zeros(N, dtype=np.uint8)
     for t in (0, M // 3, M - 2, M - 1):
         want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t), full)
