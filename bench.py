@@ -128,6 +128,11 @@ def make_stream(cfg: str, world: int, lam_override: float = 0.0):
     return sym
 
 
+def synth_histogram(sym):
+    import synth
+    return synth.histogram(sym)  # chunked: no 8-byte-per-symbol temporary at the 8 GiB config
+
+
 def cpu_oracle_decode_rate(container: np.ndarray, sample_tasks: int | None, reps: int = 1):
     """Time the oracle (plain C, single thread) decoding `sample_tasks` evenly spaced tasks
     (None = every task).  Returns (GB/s, symbols per rep, seconds per rep, description)."""
@@ -217,7 +222,7 @@ def run_reference(args, rank, world):
     import oracle  # noqa: F401
     from paper_2306_12141_b200 import recoil as R
     sym = make_stream(args.config, world, args.lam)
-    f = R.recoil_build_model(np.bincount(sym, minlength=256).astype(np.uint64), 11)
+    f = R.recoil_build_model(synth_histogram(sym), 11)
     # same split count as our arm: waves x 48 resident warps/SM (the decode kernel's occupancy at n = 11)
     # x SMs per GPU; the SM count is read from torch, not from our library
     import torch
@@ -300,7 +305,7 @@ def main():
     t_setup = time.perf_counter()
     sym = make_stream(args.config, world, args.lam)
     N_total = len(sym)
-    hist = np.bincount(sym, minlength=256).astype(np.uint64)
+    hist = synth_histogram(sym)
     f = R.recoil_build_model(hist, 11)
     warps, sms = R.recoil_decode_occupancy(local, 11)
     if not args.waves:

@@ -172,7 +172,11 @@ def workload(kind: str, n: int, seed: int, lam: float = 50.0) -> np.ndarray:
 
 
 def histogram(sym: np.ndarray) -> np.ndarray:
-    return np.bincount(sym, minlength=256).astype(np.uint64)
+    # chunked: np.bincount widens its input to intp (8 bytes per symbol at once otherwise)
+    h = np.zeros(256, np.uint64)
+    for i in range(0, len(sym), 1 << 26):
+        h += np.bincount(sym[i:i + (1 << 26)], minlength=256).astype(np.uint64)
+    return h
 
 
 # --- latent workload: 16-bit symbols with index-keyed Gaussian models -------------------
