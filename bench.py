@@ -191,8 +191,7 @@ def adaptive_extra(args, local, stream, timed_decode, peak):
     f = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
     models = {"base": h["base"], "len": h["len"], "f": f}
     K = len(h["len"])
-    table_bytes = ((K * 132 + 15) // 16 * 16 + 4 * (((int(f.size) + 3) & ~3) + K))  # plan.cpp pack_adaptive: 64 buckets per model
-    warps, sms = R.recoil_decode_occupancy_adaptive(local, table_bytes)
+    warps, sms = R.recoil_decode_occupancy_adaptive(local, K, int(f.size))
     c = R.recoil_encode_adaptive(sym, mid, models, 16, warps * sms)
     info = R.recoil_inspect(c)
     dec = R.GpuDecoder(c, local, stream=stream)

@@ -238,9 +238,13 @@ int recoil_decode_adaptive(recoil_decoder *dec, void *d_workspace, const uint16_
  * (cudaOccupancyMaxActiveBlocksPerMultiprocessor): the split count
  * that fills the GPU is warps_per_sm * sm_count * waves. */
 int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);  /* 1 <= n <= 16 */
-/* The same for the adaptive kernel with table_bytes of model tables
- * (4 (64 K + E + K) bytes for K models with E table entries). */
-int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes, int *warps_per_sm, int *sm_count);
+/* The same for the adaptive kernel of a container with n_models models and
+ * n_entries model-table entries in total (the decoded values of all models up to
+ * each model's last nonzero frequency): the plan runs 32-warp CTAs with 2^8
+ * coarse buckets per model when that layout and the tables fit one block's
+ * shared memory, else 8-warp CTAs with 2^6 buckets. */
+int recoil_decode_occupancy_adaptive(int device, uint32_t n_models, uint64_t n_entries, int *warps_per_sm,
+                                     int *sm_count);
 
 /* ---------------------------------------------------------------------- */
 /* End-to-end pipelined decode on one GPU (host container -> host symbols)  */

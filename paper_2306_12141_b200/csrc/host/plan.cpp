@@ -41,7 +41,7 @@ void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut) {
   std::memcpy(lut->data() + ((size_t)1 << n), fF, 1024);
 }
 
-int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout, uint32_t *Eout) {
+int pack_adaptive(const Container &c, uint32_t cbits, std::vector<uint8_t> *blob, uint32_t *Kout, uint32_t *Eout) {
   const uint32_t K = c.K, n = c.n;
   // per model: entries up to the last value with f > 0 (trailing zero-f values
   // cannot be decoded and would carry F = 2^n, which does not fit 16 bits)
@@ -58,10 +58,10 @@ int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *Kout
   const uint32_t E = off[K];
   if (E > 65535) return RECOIL_E_UNSUPPORTED;
   const uint32_t Epad = (E + 3) & ~3u;
-  // 64 coarse buckets per model: the u16 entry index containing each bucket's
-  // first slot, 65 boundaries (+1 pad) per model; bucket b's entries lie in
+  // 2^cbits coarse buckets per model: the u16 entry index containing each
+  // bucket's first slot, 2^cbits + 1 boundaries (+1 pad) per model; bucket b's entries lie in
   // [lo[b], lo[b+1]] (a superset by at most one entry, excluded by the search)
-  constexpr uint32_t cbits = 6, nbk = 1u << cbits, crow = nbk + 2;
+  const uint32_t nbk = 1u << cbits, crow = coarse_row(cbits);
   const size_t cwords = ((size_t)K * crow * 2 + 15) / 16 * 4;  // u16 rows, 16-B aligned
   std::vector<uint32_t> w(cwords + Epad + K, 0);
   uint16_t *coarse = reinterpret_cast<uint16_t *>(w.data());
@@ -109,7 +109,11 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   const Container &c = *d->c;
   d->fused = true;
   if (c.adaptive) {
-    int rc0 = pack_adaptive(c, &d->lut, &d->ad_K, &d->ad_E);
+    // 8-bit buckets on the 32-warp kernel when its layout and those tables fit one
+    // block's shared memory, else 6-bit buckets on the 8-warp kernel
+    int rc0 = pack_adaptive(c, kCoarseBitsWide, &d->lut, &d->ad_K, &d->ad_E);
+    d->ad_narrow = kAdaptiveWideLayoutBytes + d->lut.size() > kSmemOptinBytes;
+    if (!rc0 && d->ad_narrow) rc0 = pack_adaptive(c, kCoarseBitsNarrow, &d->lut, &d->ad_K, &d->ad_E);
     if (rc0) return rc0;
   } else {
     pack_lut(c.f, c.n, &d->lut);

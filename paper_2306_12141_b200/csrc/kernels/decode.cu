@@ -287,12 +287,13 @@ struct Warp {
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
     if constexpr (NB <= 0) {
       // Eq. 2 under model mid(i) (P:227 item (3)): the entry j of the model
-      // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (64 buckets of
+      // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (2^8 or 2^6 buckets of
       // the slot range per model) and a warp-converged binary search inside
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
       const uint32_t slot = x & ((1u << nb) - 1);
-      const uint32_t ca = coarse32 + 2 * (km * 66 + (slot >> cshift));
+      constexpr uint32_t kRow = coarse_row(NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow);
+      const uint32_t ca = coarse32 + 2 * (km * kRow + (slot >> cshift));
       uint32_t lo = lds_u16(ca), hi = lds_u16(ca + 2);
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   }
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB <= 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
-    const uint32_t words = (p.ad_K * 66 * 2 + 15) / 16 * 4 + ((p.ad_E + 3) & ~3u) + p.ad_K;
+    const uint32_t words = (uint32_t)(adaptive_table_bytes(p.ad_K, p.ad_E, NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow) / 4);
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
@@ -452,10 +453,11 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
-    w.ent32 = w.coarse32 + (p.ad_K * 66 * 2 + 15) / 16 * 16;
+    w.ent32 = w.coarse32 + (p.ad_K * coarse_row(NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow) * 2 + 15) / 16 * 16;
     w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
     w.nb = p.nbits;
-    w.cshift = p.nbits > 6 ? p.nbits - 6 : 0;
+    constexpr uint32_t cb = NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow;
+    w.cshift = p.nbits > cb ? p.nbits - cb : 0;
     w.kmax = p.ad_K - 1;
   }
   if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
@@ -844,27 +846,17 @@ static int occupancy(dev::KernelFn fn, int threads, size_t dyn, int *blocks_per_
   return RECOIL_OK;
 }
 
-// Adaptive kernels: 32-warp CTAs (NB = 0) when their layout plus the model tables
-// fit the opt-in shared memory of one block, else 8-warp CTAs (NB = -1).
-static int adaptive_narrow(size_t table_bytes, int *narrow) {
-  int dev_id = 0, optin = 0;
-  if (cudaGetDevice(&dev_id) != cudaSuccess ||
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id) != cudaSuccess)
-    return RECOIL_E_CUDA;
-  *narrow = layout_bytes(0) + table_bytes > (size_t)optin;
-  return RECOIL_OK;
-}
+// The plan (build_fused) picks the adaptive kernel: 32-warp CTAs with 8-bit coarse
+// buckets (NB = 0) when that layout and the tables fit kSmemOptinBytes, else 8-warp
+// CTAs with 6-bit buckets (NB = -1); ensure_dyn checks the device's real limit.
+}  // namespace recoil
+const uint64_t recoil::kAdaptiveWideLayoutBytes = recoil::dev::Smem<0>::kBytes;
+namespace recoil {
 
 static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *d_mid, uint8_t *d_out,
                   cudaStream_t s) {
   const recoil_plan &pl = d->plan;
   const bool adaptive = d->c->adaptive;
-  if (adaptive && d->blocks_per_sm == 0) {  // 32-warp CTAs unless the model tables leave no room
-    int narrow = 0;
-    int rc = adaptive_narrow(d->lut.size(), &narrow);
-    if (rc) return rc;
-    d->ad_narrow = narrow != 0;
-  }
   dev::KernelFn fn = dev::kernel_for(pl.prob_bits, d->fused, adaptive, d->ad_narrow);
   const int warps = adaptive ? (d->ad_narrow ? dev::warps_per_block<-1>() : dev::warps_per_block<0>())
                              : dev::warps_per_block<11>();
@@ -1046,19 +1038,22 @@ extern "C" int recoil_decoder_launches(const recoil_decoder *dec) {
   return (d->plan.n_tasks == 0 || d->single_symbol >= 0) ? 0 : 1;
 }
 
-extern "C" int recoil_decode_occupancy_adaptive(int device, uint64_t table_bytes, int *warps_per_sm,
-                                                int *sm_count) {
+extern "C" int recoil_decode_occupancy_adaptive(int device, uint32_t n_models, uint64_t n_entries,
+                                                int *warps_per_sm, int *sm_count) {
   int prev = 0;
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
-  int per_sm = 0, sms = 0, narrow = 0;
-  int rc = adaptive_narrow((size_t)table_bytes, &narrow);
+  int per_sm = 0, sms = 0, rc;
+  // the plan's choice (build_fused): 32-warp CTAs with 8-bit buckets if they fit
+  const uint64_t wide = adaptive_table_bytes(n_models, n_entries, kCoarseBitsWide);
+  const bool narrow = kAdaptiveWideLayoutBytes + wide > kSmemOptinBytes;
   const int warps = narrow ? dev::warps_per_block<-1>() : dev::warps_per_block<0>();
-  if (!rc)
-    rc = narrow ? occupancy(dev::kernel_for(16, true, true, true), dev::threads_per_block<-1>(),
-                            layout_bytes(-1) + (size_t)table_bytes, &per_sm)
-                : occupancy(dev::kernel_for(16, true, true, false), dev::threads_per_block<0>(),
-                            layout_bytes(0) + (size_t)table_bytes, &per_sm);
+  if (narrow)
+    rc = occupancy(dev::kernel_for(16, true, true, true), dev::threads_per_block<-1>(),
+                   layout_bytes(-1) + adaptive_table_bytes(n_models, n_entries, kCoarseBitsNarrow), &per_sm);
+  else
+    rc = occupancy(dev::kernel_for(16, true, true, false), dev::threads_per_block<0>(), layout_bytes(0) + wide,
+                   &per_sm);
   cudaError_t e2 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaSetDevice(prev);
   if (rc) return rc;

@@ -18,6 +18,25 @@ constexpr uint32_t kBlockBytes = 512;    // device output block: 16 groups x 32 
 constexpr uint32_t kMaxGpuProbBits = 16; // GPU decode: packed u32 LUT up to n = 12, split tables above
 constexpr uint32_t kNoFinals = 0xFFFFFFFFu;
 constexpr int64_t kNoEndCheck = INT64_MIN;
+// Adaptive model tables: per model 2^cbits coarse slot buckets, a row of 2^cbits + 2
+// u16 entry indices (2^cbits + 1 boundaries + 1 pad).  The 32-warp adaptive kernel
+// uses 8 bits (fewer binary-search steps: 2^25 latent symbols 193 -> 248 G
+// symbols/s against 6 bits); the 8-warp fallback for large model sets uses 6.
+constexpr uint32_t kCoarseBitsWide = 8, kCoarseBitsNarrow = 6;
+#ifdef __CUDACC__
+#define RECOIL_HD __host__ __device__
+#else
+#define RECOIL_HD
+#endif
+RECOIL_HD constexpr uint32_t coarse_row(uint32_t cbits) { return (1u << cbits) + 2; }
+// Bytes of the packed adaptive tables (pack_adaptive) for K models, E entries.
+RECOIL_HD constexpr uint64_t adaptive_table_bytes(uint32_t K, uint64_t E, uint32_t cbits) {
+  return ((uint64_t)K * coarse_row(cbits) * 2 + 15) / 16 * 16 + 4 * (((E + 3) & ~3ull) + K);
+}
+// Shared-memory layout bytes of the 32-warp adaptive kernel and the opt-in limit it
+// is planned against (sm_100: 227 KB per block); decode.cu checks both at run time.
+extern const uint64_t kAdaptiveWideLayoutBytes;
+constexpr uint64_t kSmemOptinBytes = 232448;
 
 // Parsed container of either kind. Recoil: M tasks, M-1 split points.
 // Partitioned: M partitions (tasks), no points.
@@ -133,7 +152,7 @@ void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
 // boundaries (entry holding each of the 64 buckets' first slot, + end, + pad;
 // 16-B aligned), E entries F | (f-1) << 16 (padded to 4), K value offsets.
 // E_UNSUPPORTED if E > 65535.
-int pack_adaptive(const Container &c, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
+int pack_adaptive(const Container &c, uint32_t cbits, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
 
 
 }  // namespace recoil

@@ -105,7 +105,7 @@ def load(path: str = LIB_PATH):
         "recoil_quantize": (i32, [P, u32, u32, P]),
         "recoil_encode_adaptive": (i32, [P, u64, P, u32, P, P, P, u32, u32, P, P]),
         "recoil_decode_adaptive": (i32, [P, P, P, P, P, P]),
-        "recoil_decode_occupancy_adaptive": (i32, [i32, u64, P, P]),
+        "recoil_decode_occupancy_adaptive": (i32, [i32, u32, u64, P, P]),
         "recoil_decoder_create_subset": (i32, [P, u64, u32, u64, u64, P]),
         "recoil_decoder_create_grouped": (i32, [P, u64, u32, P, P, P]),
     }
@@ -309,9 +309,11 @@ def recoil_decode_adaptive(handle, d_workspace: int, d_words: int, d_model_ids: 
            "recoil_decode_adaptive")
 
 
-def recoil_decode_occupancy_adaptive(device: int, table_bytes: int) -> tuple[int, int]:
+def recoil_decode_occupancy_adaptive(device: int, n_models: int, n_entries: int) -> tuple[int, int]:
+    """(resident warps per SM, SMs) of the adaptive kernel for n_models models with n_entries
+    table entries in total (an upper bound such as the model set's total value count is fine)."""
     w, s = ctypes.c_int(0), ctypes.c_int(0)
-    _check(load().recoil_decode_occupancy_adaptive(device, table_bytes, ctypes.byref(w), ctypes.byref(s)),
+    _check(load().recoil_decode_occupancy_adaptive(device, n_models, n_entries, ctypes.byref(w), ctypes.byref(s)),
            "recoil_decode_occupancy_adaptive")
     return w.value, s.value
 

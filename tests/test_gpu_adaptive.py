@@ -155,10 +155,10 @@ def test_large_model_tables_use_narrow_ctas(K, length):
         ln.append(length)
         fs.append(oracle.quantize(hist, 16))
     models = {"base": np.array(base, np.uint32), "len": np.array(ln, np.uint32), "f": np.concatenate(fs)}
-    table_bytes = (K * 132 + 15) // 16 * 16 + 4 * (((K * length + 3) & ~3) + K)
+    table_bytes = (K * 258 * 2 + 15) // 16 * 16 + 4 * (K * length + K)  # 8-bit coarse buckets
     assert table_bytes > 105_000  # the 32-warp layout (125 KB) leaves ~102 KB of the 227 KB
-    warps, _ = R.recoil_decode_occupancy_adaptive(0, table_bytes)
-    assert warps >= 8 and warps % 8 == 0
+    warps, _ = R.recoil_decode_occupancy_adaptive(0, K, K * length)
+    assert warps >= 8 and warps % 8 == 0 and warps != 32  # 8-warp CTAs
     sym, mid = _draw(rng, models, 300_000, K)
     c = R.recoil_encode_adaptive(sym, mid, models, 16, 64)
     _check(c, mid, sym, oracle_check=True)

@@ -7,8 +7,7 @@ N = 1 << 25
 sym, mid, h = synth.latent_workload(N, synth.seed_for(6))
 f = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
 K = len(h["len"])
-tb = ((K * 132 + 15) // 16 * 16 + 4 * (((int(f.size) + 3) & ~3) + K))
-warps, sms = R.recoil_decode_occupancy_adaptive(0, tb)
+warps, sms = R.recoil_decode_occupancy_adaptive(0, K, int(f.size))
 c = R.recoil_encode_adaptive(sym, mid, {"base": h["base"], "len": h["len"], "f": f}, 16, warps * sms)
 dec = R.GpuDecoder(c, 0)
 dec.set_model_ids(mid)
