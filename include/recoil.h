@@ -240,9 +240,9 @@ int recoil_decode_adaptive(recoil_decoder *dec, void *d_workspace, const uint16_
 int recoil_decode_occupancy(int device, uint32_t prob_bits, int *warps_per_sm, int *sm_count);  /* 1 <= n <= 16 */
 /* The same for the adaptive kernel of a container with n_models models and
  * n_entries model-table entries in total (the decoded values of all models up to
- * each model's last nonzero frequency): the plan runs 32-warp CTAs with 2^8
- * coarse buckets per model when that layout and the tables fit one block's
- * shared memory, else 8-warp CTAs with 2^6 buckets. */
+ * each model's last nonzero frequency): the plan runs 32-warp CTAs with 2^9,
+ * 2^8 or 2^7 coarse buckets per model (the most that fit beside that layout in
+ * one block's shared memory), else 8-warp CTAs with 2^6 buckets. */
 int recoil_decode_occupancy_adaptive(int device, uint32_t n_models, uint64_t n_entries, int *warps_per_sm,
                                      int *sm_count);
 

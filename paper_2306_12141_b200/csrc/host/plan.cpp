@@ -111,9 +111,17 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   if (c.adaptive) {
     // 8-bit buckets on the 32-warp kernel when its layout and those tables fit one
     // block's shared memory, else 6-bit buckets on the 8-warp kernel
-    int rc0 = pack_adaptive(c, kCoarseBitsWide, &d->lut, &d->ad_K, &d->ad_E);
-    d->ad_narrow = kAdaptiveWideLayoutBytes + d->lut.size() > kSmemOptinBytes;
-    if (!rc0 && d->ad_narrow) rc0 = pack_adaptive(c, kCoarseBitsNarrow, &d->lut, &d->ad_K, &d->ad_E);
+    int rc0 = RECOIL_OK;
+    d->ad_narrow = true;
+    for (uint32_t cb = kCoarseBitsWide; cb >= kCoarseBitsWideMin && d->ad_narrow && !rc0; --cb) {
+      rc0 = pack_adaptive(c, cb, &d->lut, &d->ad_K, &d->ad_E);
+      d->ad_cbits = cb;
+      d->ad_narrow = kAdaptiveWideLayoutBytes + d->lut.size() > kSmemOptinBytes;
+    }
+    if (!rc0 && d->ad_narrow) {
+      rc0 = pack_adaptive(c, kCoarseBitsNarrow, &d->lut, &d->ad_K, &d->ad_E);
+      d->ad_cbits = kCoarseBitsNarrow;
+    }
     if (rc0) return rc0;
   } else {
     pack_lut(c.f, c.n, &d->lut);

@@ -107,7 +107,7 @@ struct Params {
   // adaptive codec (NB = 0): model id of every symbol (absolute index, 16-B
   // aligned), model count, table entries, n
   const uint8_t *mid;
-  uint32_t ad_K, ad_E, nbits;
+  uint32_t ad_K, ad_E, nbits, ad_cbits, ad_crow;  // + coarse bucket bits, u16 row length
 };
 
 // Shared memory per block (dynamic; about 31 KB for n = 11 at 8 warps): the word
@@ -292,8 +292,7 @@ struct Warp {
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
       const uint32_t slot = x & ((1u << nb) - 1);
-      constexpr uint32_t kRow = coarse_row(NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow);
-      const uint32_t ca = coarse32 + 2 * (km * kRow + (slot >> cshift));
+      const uint32_t ca = coarse32 + 2 * (km * p->ad_crow + (slot >> cshift));
       uint32_t lo = lds_u16(ca), hi = lds_u16(ca + 2);
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
@@ -420,7 +419,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   }
   // a2: stage the LUT in shared memory (per block)
   if constexpr (NB <= 0) {  // adaptive: coarse table, entries, value offsets (p.lut blob)
-    const uint32_t words = (uint32_t)(adaptive_table_bytes(p.ad_K, p.ad_E, NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow) / 4);
+    const uint32_t words = (uint32_t)(adaptive_table_bytes(p.ad_K, p.ad_E, p.ad_cbits) / 4);
     for (uint32_t i = threadIdx.x; i < words / 4; i += kThreads)
       reinterpret_cast<int4 *>(sym_dyn)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     for (uint32_t i = (words & ~3u) + threadIdx.x; i < words; i += kThreads)
@@ -453,11 +452,10 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
-    w.ent32 = w.coarse32 + (p.ad_K * coarse_row(NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow) * 2 + 15) / 16 * 16;
+    w.ent32 = w.coarse32 + (p.ad_K * p.ad_crow * 2 + 15) / 16 * 16;
     w.delta32 = w.ent32 + 4 * ((p.ad_E + 3) & ~3u);
     w.nb = p.nbits;
-    constexpr uint32_t cb = NB == 0 ? kCoarseBitsWide : kCoarseBitsNarrow;
-    w.cshift = p.nbits > cb ? p.nbits - cb : 0;
+    w.cshift = p.nbits > p.ad_cbits ? p.nbits - p.ad_cbits : 0;
     w.kmax = p.ad_K - 1;
   }
   if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
@@ -910,6 +908,8 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.mid = d_mid;
   prm.ad_K = d->ad_K;
   prm.ad_E = d->ad_E;
+  prm.ad_cbits = d->ad_cbits;
+  prm.ad_crow = coarse_row(d->ad_cbits);
   prm.nbits = pl.prob_bits;
   // fewer tasks than resident warps: narrower blocks, so the tasks spread over
   // all SMs instead of filling a few (config 4 at 2048 splits: 86 SMs x 24 warps)
@@ -1045,8 +1045,12 @@ extern "C" int recoil_decode_occupancy_adaptive(int device, uint32_t n_models, u
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0, rc;
   // the plan's choice (build_fused): 32-warp CTAs with 8-bit buckets if they fit
-  const uint64_t wide = adaptive_table_bytes(n_models, n_entries, kCoarseBitsWide);
-  const bool narrow = kAdaptiveWideLayoutBytes + wide > kSmemOptinBytes;
+  uint64_t wide = 0;
+  bool narrow = true;
+  for (uint32_t cb = kCoarseBitsWide; cb >= kCoarseBitsWideMin && narrow; --cb) {
+    wide = adaptive_table_bytes(n_models, n_entries, cb);
+    narrow = kAdaptiveWideLayoutBytes + wide > kSmemOptinBytes;
+  }
   const int warps = narrow ? dev::warps_per_block<-1>() : dev::warps_per_block<0>();
   if (narrow)
     rc = occupancy(dev::kernel_for(16, true, true, true), dev::threads_per_block<-1>(),

@@ -20,9 +20,10 @@ constexpr uint32_t kNoFinals = 0xFFFFFFFFu;
 constexpr int64_t kNoEndCheck = INT64_MIN;
 // Adaptive model tables: per model 2^cbits coarse slot buckets, a row of 2^cbits + 2
 // u16 entry indices (2^cbits + 1 boundaries + 1 pad).  The 32-warp adaptive kernel
-// uses 8 bits (fewer binary-search steps: 2^25 latent symbols 193 -> 248 G
-// symbols/s against 6 bits); the 8-warp fallback for large model sets uses 6.
-constexpr uint32_t kCoarseBitsWide = 8, kCoarseBitsNarrow = 6;
+// takes the most bits in 9..7 whose tables fit beside its layout (fewer binary-
+// search steps: 2^25 latent symbols 193 / 248 / 275 G symbols/s at 6 / 8 / 9 bits);
+// the 8-warp fallback for large model sets uses 6.
+constexpr uint32_t kCoarseBitsWide = 9, kCoarseBitsWideMin = 7, kCoarseBitsNarrow = 6;
 #ifdef __CUDACC__
 #define RECOIL_HD __host__ __device__
 #else
@@ -133,6 +134,7 @@ struct Decoder {
   uint32_t ad_K = 0, ad_E = 0;     // adaptive: models, table entries (lut = coarse | entries | offsets)
   int blocks_per_sm = 0, sm_count = 0;  // launch geometry (occupancy API), cached
   bool ad_narrow = false;          // adaptive: 8-warp CTAs (the model tables leave no room for 32 warps)
+  uint32_t ad_cbits = 0;           // adaptive: coarse bucket bits of the packed tables
 };
 
 int build_decoder(const uint8_t *c, uint64_t len, uint64_t task_begin, uint64_t task_end, Decoder *d,
