@@ -70,6 +70,8 @@ def _load():
         "or_backward_scan": (i32, [P, u64, u32, P, P, P]),
         "or_heuristic": (i64, [i64, i64, i64]),
         "or_choose_splits": (i64, [P, u64, u64, u32, u32, P]),
+        "or_choose_splits_ex": (i64, [P, u64, u64, u32, u32, u32, P]),
+        "or_recoil_encode_ex": (i32, [P, u64, P, u32, u32, u32, u32, P, P]),
         "or_pack_series": (u64, [P, u64, i32, u32, P, u64]),
         "or_unpack_series": (i64, [P, u64, u64, u64, i32, u32, P]),
         "or_decode_from": (i32, [P, u64, P, u32, u32, u64, i64, i64, P, P, u64, u64, P, P, P]),
@@ -196,10 +198,14 @@ def heuristic(t: int, ts: int, T: int) -> int:
     return int(_load().or_heuristic(t, ts, T))
 
 
-def choose_splits(events, N: int, W: int, M: int) -> np.ndarray:
+SPLIT_PRINTED_T = 1  # or_choose_splits_ex flag: T = ceil(N/M) as printed, not reading Z10''s T_m
+
+
+def choose_splits(events, N: int, W: int, M: int, printed_T: bool = False) -> np.ndarray:
     ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
     chosen = np.zeros(max(M, 1), dtype=np.uint64)
-    k = _check(_load().or_choose_splits(_ptr(ev), ev.size, N, W, M, chosen.ctypes.data))
+    k = _check(_load().or_choose_splits_ex(_ptr(ev), ev.size, N, W, M, SPLIT_PRINTED_T if printed_T else 0,
+                                           chosen.ctypes.data))
     return chosen[:k].copy()
 
 
@@ -242,9 +248,10 @@ def _sized_call(fn, *args) -> bytes:
     return out[: ln.value].tobytes()
 
 
-def recoil_encode(sym, f, n: int, M: int, W: int = 32) -> bytes:
+def recoil_encode(sym, f, n: int, M: int, W: int = 32, printed_T: bool = False) -> bytes:
     s = _u8(sym)
-    return _sized_call(_load().or_recoil_encode, _ptr(s), s.size, _freqs(f).ctypes.data, n, W, M)
+    return _sized_call(_load().or_recoil_encode_ex, _ptr(s), s.size, _freqs(f).ctypes.data, n, W, M,
+                       SPLIT_PRINTED_T if printed_T else 0)
 
 
 def combine(container: bytes, target: int) -> bytes:

@@ -289,6 +289,13 @@ int64_t or_heuristic(int64_t t, int64_t ts, int64_t T) { return iabs64(t - T) + 
  * fewer splits. */
 int64_t or_choose_splits(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t W, uint32_t M,
                          uint64_t *chosen) {
+  return or_choose_splits_ex(ev, n_ev, N, W, M, 0, chosen);
+}
+
+/* flags & OR_SPLIT_PRINTED_T: the printed T = ceil(N/M) of P:329 for every
+ * boundary instead of Z10''s T_m (kept to compare the two readings). */
+int64_t or_choose_splits_ex(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t W, uint32_t M,
+                            uint32_t flags, uint64_t *chosen) {
   if (M <= 1 || N == 0) return 0;
   int64_t prev = -1;
   int64_t count = 0;
@@ -296,7 +303,8 @@ int64_t or_choose_splits(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t
   uint32_t st[32];
   int64_t ai[32];
   for (uint32_t m = 1; m < M; ++m) {
-    int64_t T = (int64_t)ceil_div(N - (uint64_t)(prev + 1), M - m + 1);
+    int64_t T = (flags & OR_SPLIT_PRINTED_T) ? (int64_t)ceil_div(N, M)
+                                             : (int64_t)ceil_div(N - (uint64_t)(prev + 1), M - m + 1);
     while (first < n_ev && ev[first].idx <= prev) first++;
     int64_t best = -1, best_h = 0;
     /* candidates with 0 < t <= 2T; a window without a feasible candidate is
@@ -701,6 +709,11 @@ static void point_span(const or_box *bx, uint64_t k, int64_t *ss, int64_t *bidx)
 
 int or_recoil_encode(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
                      uint32_t W, uint32_t M, uint8_t *out, uint64_t *len) {
+  return or_recoil_encode_ex(sym, N, f, n, W, M, 0, out, len);
+}
+
+int or_recoil_encode_ex(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
+                        uint32_t W, uint32_t M, uint32_t split_flags, uint8_t *out, uint64_t *len) {
   if (M < 1 || W < 1 || W > 32 || n < 1 || n > 16) return OR_E_ARG;
   uint64_t fs = 0;
   for (int s = 0; s < 256; ++s) fs += f[s];
@@ -719,7 +732,7 @@ int or_recoil_encode(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint
   if (B < 0) { free(words); free(ev); return (int)B; }
   bx.B = (uint64_t)B;
   uint64_t *chosen = (uint64_t *)malloc(8ull * M);
-  int64_t P = or_choose_splits(ev, bx.B, N, W, M, chosen);
+  int64_t P = or_choose_splits_ex(ev, bx.B, N, W, M, split_flags, chosen);
   bx.M = (uint32_t)P + 1;
   bx.offset = (uint64_t *)calloc((uint64_t)P + 1, 8);
   bx.maxg = (uint64_t *)calloc((uint64_t)P + 1, 8);
@@ -1202,7 +1215,7 @@ int or_ad_recoil_encode(const uint16_t *sym, uint64_t N, const uint8_t *mid, uin
   memcpy(bx.mlen, len, 4ull * K);
   memcpy(bx.mf, mf, 4 * msum);
   bx.B = (uint64_t)B;
-  int64_t P = or_choose_splits(ev, bx.B, N, W, M, chosen);
+  int64_t P = or_choose_splits_ex(ev, bx.B, N, W, M, 0, chosen);
   bx.M = (uint32_t)P + 1;
   bx.offset = (uint64_t *)calloc((uint64_t)P + 1, 8);
   bx.maxg = (uint64_t *)calloc((uint64_t)P + 1, 8);

@@ -64,6 +64,11 @@ int64_t or_heuristic(int64_t t, int64_t ts, int64_t T);
 /* Split selection (reading Z10): writes chosen event offsets, returns count. */
 int64_t or_choose_splits(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t W, uint32_t M,
                          uint64_t *chosen);
+/* The same with flags: OR_SPLIT_PRINTED_T = T fixed at the printed ceil(N/M)
+ * instead of reading Z10''s per-boundary T_m. */
+#define OR_SPLIT_PRINTED_T 1u
+int64_t or_choose_splits_ex(const or_event *ev, uint64_t n_ev, uint64_t N, uint32_t W, uint32_t M,
+                            uint32_t flags, uint64_t *chosen);
 
 /* Data series: bit-packed, MSB first. */
 uint64_t or_pack_series(const int64_t *v, uint64_t count, int is_signed, uint32_t field_bits,
@@ -81,6 +86,8 @@ int or_decode_from(const uint16_t *words, uint64_t B, const uint32_t f[256], uin
 /* Whole-pipeline helpers: Recoil container. */
 int or_recoil_encode(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
                      uint32_t W, uint32_t M, uint8_t *out, uint64_t *len);
+int or_recoil_encode_ex(const uint8_t *sym, uint64_t N, const uint32_t f[256], uint32_t n,
+                        uint32_t W, uint32_t M, uint32_t split_flags, uint8_t *out, uint64_t *len);
 int or_combine(const uint8_t *in, uint64_t in_len, uint32_t target, uint8_t *out, uint64_t *len);
 int or_container_info(const uint8_t *c, uint64_t len, uint64_t info[8]);
 /* split table of a container: per point (M-1): offset, max_group, sync_start, boundary idx */
