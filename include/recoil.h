@@ -158,6 +158,8 @@ typedef struct {
   uint64_t upload_bytes;         /* bytes recoil_decoder_upload copies host->device     */
   uint32_t symbol_bytes;         /* 1 (8-bit symbols) or 2 (adaptive "RCA1", uint16_t)   */
   uint32_t n_models;             /* adaptive: K models; else 1                          */
+  uint32_t coarse_bits;          /* adaptive: coarse slot buckets per model = 2^coarse_bits; else 0 */
+  uint32_t warps_per_block;      /* the decode kernel's CTA size for this plan (warps)  */
 } recoil_plan;
 
 /* Host half of the path (DESIGN.md row a1): parse the container

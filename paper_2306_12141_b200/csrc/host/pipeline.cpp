@@ -41,6 +41,7 @@ struct Pipeline {
   std::vector<uint64_t> bounds;
   std::vector<Decoder> dec;        // the last run's chunk plans (alive until status)
   int single_symbol = -1;
+  uint32_t prev_streams = 0;       // buffer sets the previous run used (its work may still be queued)
 
   ~Pipeline() {
     for (auto &p : staging)
@@ -122,6 +123,12 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
   Pipeline *pl = reinterpret_cast<Pipeline *>(p);
   if (pl->N && !host_out) return RECOIL_E_ARG;
   try {
+    // a previous run enqueued without an intervening status call may still be
+    // reading its buffer sets, staging and status words: wait for its last D2H per
+    // set (each set's work is chained, so that event follows all of it)
+    for (uint32_t s = 0; s < pl->prev_streams; ++s)
+      if (pl->ev_out[s] && cudaEventSynchronize(pl->ev_out[s]) != cudaSuccess) return RECOIL_E_CUDA;
+    pl->prev_streams = 0;
     // per run: parse and plan again (this is the host half of the path)
     auto c = std::make_shared<Container>();
     int rc = parse_container(pl->bytes, pl->len, c.get(), /*light=*/true);
@@ -145,6 +152,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
     cudaStream_t sc = reinterpret_cast<cudaStream_t>(streams[std::min<uint32_t>(1, n_streams - 1)]);
     cudaStream_t so = reinterpret_cast<cudaStream_t>(streams[std::min<uint32_t>(2, n_streams - 1)]);
     std::memset(pl->status, 0, sizeof(DeviceStatus) * pl->chunks);
+    pl->prev_streams = std::min<uint32_t>(n_streams, pl->chunks);
     for (uint32_t k = 0; k < pl->chunks; ++k) {
       const uint32_t s = k % n_streams;
       cudaStream_t st = sh;
@@ -214,7 +222,8 @@ extern "C" int recoil_pipeline_status(recoil_pipeline *p, void *const *streams, 
     const DeviceStatus &st = pl->status[k];
     if (st.bad_task) bad = std::min<uint64_t>(bad, 0xFFFFFFFFu - st.bad_task);
     if (st.flags & 4u) rc = RECOIL_E_INCONSISTENT;
-    else if ((st.flags & 1u) && rc != RECOIL_E_INCONSISTENT) rc = RECOIL_E_UNDERFLOW;
+    else if ((st.flags & 8u) && rc != RECOIL_E_INCONSISTENT) rc = RECOIL_E_UNSUPPORTED;
+    else if ((st.flags & 1u) && rc != RECOIL_E_INCONSISTENT && rc != RECOIL_E_UNSUPPORTED) rc = RECOIL_E_UNDERFLOW;
     else if ((st.flags & 2u) && rc == RECOIL_OK) rc = RECOIL_E_SYNC;
   }
   if (bad_task) *bad_task = bad;

@@ -201,6 +201,8 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   p.n_tasks = d->n_tasks;
   p.symbol_bytes = c.adaptive ? 2 : 1;
   p.n_models = c.adaptive ? c.K : 1;
+  p.coarse_bits = c.adaptive ? d->ad_cbits : 0;
+  p.warps_per_block = c.adaptive ? (d->ad_narrow ? kWarpsAdaptiveNarrow : kWarpsAdaptive) : kWarpsStatic;
   d->lut_off = 16;
   d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());
@@ -327,6 +329,7 @@ int build_decoder_from(std::shared_ptr<const Container> cptr, uint64_t task_begi
   uint64_t write_end = p.out_hi;
   for (const TaskRec &r : d->tasks) write_end = std::max(write_end, r.write_hi);
   p.out_count = ((write_end + 15) & ~15ull) - p.out_base;
+  p.warps_per_block = kWarpsStatic;
   d->lut_off = 16;
   d->finals_off = align16(d->lut_off + d->lut.size());
   d->tasks_off = align16(d->finals_off + 4 * d->finals.size());

@@ -46,13 +46,13 @@ namespace dev {
 // rank 0..5 of an SM at 8 warps took 55 / 59 / 66 / 77 / 90 / 101 us of a 104 us
 // decode, warps of one CTA alike).  So the static kernels run 2 CTAs of 24 warps
 // (48 warps per SM, two priority levels; config 2: 989 -> 1082 GB/s, config 3
-// 1277 -> 1324); the adaptive kernel, whose model tables take 23 KB more per
-// CTA, keeps 8-warp CTAs (4 per SM).
+// 1277 -> 1324); the adaptive kernel runs one CTA of 32 warps (8-warp CTAs
+// when its model tables leave no room for that layout).
 #ifndef RECOIL_WARPS
-#define RECOIL_WARPS 24
+#define RECOIL_WARPS kWarpsStatic
 #endif
 #ifndef RECOIL_WARPS_ADAPTIVE
-#define RECOIL_WARPS_ADAPTIVE 32
+#define RECOIL_WARPS_ADAPTIVE kWarpsAdaptive
 #endif
 // NB = 0 and NB = -1 are the adaptive codec (NEXT rows 1 + 4: index-keyed
 // models, 16-bit symbols, n at run time; model tables in dynamic shared memory):
@@ -61,7 +61,7 @@ namespace dev {
 // layout, 8-warp CTAs (NB = -1).
 template <int NB>
 __host__ __device__ constexpr int warps_per_block() {
-  return NB == 0 ? RECOIL_WARPS_ADAPTIVE : NB < 0 ? 8 : RECOIL_WARPS;
+  return NB == 0 ? (int)RECOIL_WARPS_ADAPTIVE : NB < 0 ? (int)kWarpsAdaptiveNarrow : (int)RECOIL_WARPS;
 }
 template <int NB>
 __host__ __device__ constexpr int threads_per_block() { return 32 * warps_per_block<NB>(); }
@@ -98,6 +98,7 @@ struct Params {
   const uint16_t *words;  // slice base (stream word word_lo)
   uint8_t *out;           // symbol out_base
   uint64_t out_base;
+  uint64_t out_lim;       // out_base + out_count: no task writes at or beyond this symbol
   int32_t n_chunks;       // slice words / 256
   uint32_t n_tasks;
   // Runtime constants, opaque to ptxas, that keep some steady-state work on the
@@ -321,8 +322,10 @@ struct Warp {
   // a8: write an output block: every 16-B chunk of this lane inside the task's
   // write window [woff, wend) (offsets relative to the block's base `dst`).
   // S = symbol bytes: each lane writes 16 S bytes (its part of the 512-symbol block)
+  // Offsets are unsigned 32-bit: a task's write window spans < 2^32 - 1024 bytes
+  // (checked per task; longer tasks flag E_UNSUPPORTED).
   template <int S>
-  __device__ __forceinline__ void flush_at(uint8_t *dst, int c, int woff, int wend) {
+  __device__ __forceinline__ void flush_at(uint8_t *dst, uint32_t c, uint32_t woff, uint32_t wend) {
     __syncwarp();
     if (c >= woff && c + 16 * S <= wend) {
       const uint32_t a = stage32 + (16 * S - S) * lane;  // staging base + 16 S lane
@@ -332,7 +335,7 @@ struct Warp {
     __syncwarp();  // the staging block is rewritten by the next group steps
   }
   template <int S>
-  __device__ __forceinline__ void flush(uint8_t *dst, int rel, int woff, int wend) {
+  __device__ __forceinline__ void flush(uint8_t *dst, uint32_t rel, uint32_t woff, uint32_t wend) {
     flush_at<S>(dst, rel + 16 * S * lane, woff, wend);
   }
 };
@@ -612,14 +615,30 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     cp_wait<1>();
     __syncwarp();
 
+    // The task's write window [32 group(lo), whi) must lie inside the plan's output
+    // buffer [out_base, out_lim) and its first group inside the stream; a record
+    // that says otherwise (corrupt or crafted metadata) is flagged, not decoded.
+    // Windows of 2^32 - 1024 bytes or more exceed the 32-bit block offsets: E_UNSUPPORTED.
+    if (start_group >= 0) {
+      const bool bad_win = start_group >= p.G || (lo & ~31ull) < p.out_base || whi > p.out_lim || whi <= lo;
+      const bool too_long = !bad_win && (whi - (lo & ~511ull)) * S >= 0xFFFFFC00ull;
+      if (bad_win || too_long) {
+        if (lane == 0) {
+          atomicOr(&p.status->flags, bad_win ? 4u : 8u);
+          atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
+        }
+        lo = 0;
+        start_group = -1;
+      }
+    }
     const int32_t lo_group = (int32_t)(lo >> 5);
     const int32_t min_init = __reduce_min_sync(kFull, init_group);
     const int32_t g_sync_end = max(min_init, lo_group);
     // 32-bit output bookkeeping relative to the block of lo_group (bytes: S per symbol)
     const int32_t b_lo = lo_group >> 4;
     uint8_t *const out_blo = p.out + ((uint64_t)b_lo * kBlockBytes - p.out_base) * S;
-    const int woff = (lo_group & 15) * (int)kLanes * S;  // 0..511 symbols into block b_lo
-    const int wend = (int)(whi - (uint64_t)b_lo * kBlockBytes) * S;
+    const uint32_t woff = (lo_group & 15) * kLanes * S;  // 0..511 symbols into block b_lo
+    const uint32_t wend = (uint32_t)((whi - (uint64_t)b_lo * kBlockBytes) * S);
     constexpr int kBlk = (int)kBlockBytes * S;  // output block bytes
 
     // adaptive: the model ids of the block being decoded are staged in shared
@@ -660,7 +679,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       x = run_part<NB, true>(w, lut, sym, x, g, ge, init_group, state);
       if (ge == gb) {
         const int rel = (gb >> 4) - b_lo;
-        w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
+        w.template flush<S>(out_blo + (uint32_t)rel * kBlk, (uint32_t)rel * kBlk, woff, wend);
       }
       g = ge - 1;
     }
@@ -670,7 +689,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       if (g == start_group) stage_block(g >> 4);  // else staged by the sync phase
       x = run_part<NB, false>(w, lut, sym, x, g, ge, 0, 0);
       const int rel = (gb >> 4) - b_lo;
-      w.template flush<S>(out_blo + rel * kBlk, rel * kBlk, woff, wend);
+      w.template flush<S>(out_blo + (uint32_t)rel * kBlk, (uint32_t)rel * kBlk, woff, wend);
       g = ge - 1;
     }
     if (g >= lo_group) {
@@ -678,8 +697,8 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       // three blocks before the end
       int rel = (g >> 4) - b_lo;
       const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      uint8_t *dst = out_blo + rel * kBlk;
-      int c = rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
+      uint8_t *dst = out_blo + (uint32_t)rel * kBlk;
+      uint32_t c = (uint32_t)rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
       for (; rel >= full_lo + 3; --rel) {
         stage_block(b_lo + rel);
         x = run_block<NB>(w, lut, sym, x);
@@ -844,9 +863,9 @@ static int occupancy(dev::KernelFn fn, int threads, size_t dyn, int *blocks_per_
   return RECOIL_OK;
 }
 
-// The plan (build_fused) picks the adaptive kernel: 32-warp CTAs with 8-bit coarse
-// buckets (NB = 0) when that layout and the tables fit kSmemOptinBytes, else 8-warp
-// CTAs with 6-bit buckets (NB = -1); ensure_dyn checks the device's real limit.
+// The plan (build_fused) picks the adaptive kernel: 32-warp CTAs with the most coarse
+// bucket bits in 9..7 (NB = 0) whose tables fit beside that layout in kSmemOptinBytes,
+// else 8-warp CTAs with 6-bit buckets (NB = -1); ensure_dyn checks the device's real limit.
 }  // namespace recoil
 const uint64_t recoil::kAdaptiveWideLayoutBytes = recoil::dev::Smem<0>::kBytes;
 namespace recoil {
@@ -901,6 +920,7 @@ static int launch(Decoder *d, char *ws, const uint16_t *d_words, const uint8_t *
   prm.words = d_words;
   prm.out = d_out;
   prm.out_base = pl.out_base;
+  prm.out_lim = pl.out_base + pl.out_count;
   prm.n_chunks = (int32_t)(pl.word_count / kChunkWords);
   prm.n_tasks = pl.n_tasks;
   prm.neg2 = -2;
@@ -1027,6 +1047,7 @@ extern "C" int recoil_decoder_status(recoil_decoder *dec, const void *d_workspac
   if (cudaStreamSynchronize(s) != cudaSuccess) return RECOIL_E_CUDA;
   if (bad) *bad = st.bad_task ? (uint64_t)(0xFFFFFFFFu - st.bad_task) : UINT64_MAX;
   if (st.flags & 4u) return RECOIL_E_INCONSISTENT;
+  if (st.flags & 8u) return RECOIL_E_UNSUPPORTED;
   if (st.flags & 1u) return RECOIL_E_UNDERFLOW;
   if (st.flags & 2u) return RECOIL_E_SYNC;
   return RECOIL_OK;

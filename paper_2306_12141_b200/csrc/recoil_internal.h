@@ -24,6 +24,9 @@ constexpr int64_t kNoEndCheck = INT64_MIN;
 // search steps: 2^25 latent symbols 193 / 248 / 275 G symbols/s at 6 / 8 / 9 bits);
 // the 8-warp fallback for large model sets uses 6.
 constexpr uint32_t kCoarseBitsWide = 9, kCoarseBitsWideMin = 7, kCoarseBitsNarrow = 6;
+// Decode kernel CTA sizes in warps (decode.cu): static codec 2 CTAs x 24 per SM;
+// adaptive one CTA of 32, or 8-warp CTAs when the model tables need the room.
+constexpr uint32_t kWarpsStatic = 24, kWarpsAdaptive = 32, kWarpsAdaptiveNarrow = 8;
 #ifdef __CUDACC__
 #define RECOIL_HD __host__ __device__
 #else
@@ -111,7 +114,8 @@ static_assert(sizeof(TaskHead) == 32, "TaskHead layout");
 constexpr uint32_t kHeadLast = 1, kHeadFirst = 2;
 
 struct DeviceStatus {   // first 16 B of the workspace, zeroed before every decode
-  uint32_t flags;       // bit 0 underflow, bit 1 end-state mismatch, bit 2 inconsistent metadata
+  uint32_t flags;       // bit 0 underflow, bit 1 end-state mismatch, bit 2 inconsistent metadata,
+                        // bit 3 a task window too long for the 32-bit block offsets (E_UNSUPPORTED)
   uint32_t bad_task;    // atomicMax of (0xFFFFFFFF - failing task id); 0 = none
   uint32_t next_task;   // persistent-warp task counter
   uint32_t pad;
@@ -150,9 +154,10 @@ void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
 void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,
                         uint64_t *bounds);
 void pack_lut(const uint32_t f[256], uint32_t n, std::vector<uint8_t> *lut);
-// Adaptive model tables for the GPU: K x 66 u16 coarse bucket
-// boundaries (entry holding each of the 64 buckets' first slot, + end, + pad;
-// 16-B aligned), E entries F | (f-1) << 16 (padded to 4), K value offsets.
+// Adaptive model tables for the GPU: K rows of 2^cbits + 2 u16
+// coarse bucket boundaries (entry holding each of the 2^cbits buckets' first slot,
+// + end, + pad; 16-B aligned), E entries F | (f-1) << 16 (padded to 4), K value
+// offsets.  cbits is chosen per plan: 9..7 on the 32-warp kernel, 6 on the 8-warp one.
 // E_UNSUPPORTED if E > 65535.
 int pack_adaptive(const Container &c, uint32_t cbits, std::vector<uint8_t> *blob, uint32_t *K, uint32_t *E);
 

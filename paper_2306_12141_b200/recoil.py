@@ -62,7 +62,8 @@ class recoil_plan(ctypes.Structure):
                 ("prob_bits", ctypes.c_uint32), ("word_lo", ctypes.c_uint64), ("word_count", ctypes.c_uint64),
                 ("out_lo", ctypes.c_uint64), ("out_hi", ctypes.c_uint64), ("out_base", ctypes.c_uint64),
                 ("out_count", ctypes.c_uint64), ("workspace_bytes", ctypes.c_uint64),
-                ("upload_bytes", ctypes.c_uint64), ("symbol_bytes", ctypes.c_uint32), ("n_models", ctypes.c_uint32)]
+                ("upload_bytes", ctypes.c_uint64), ("symbol_bytes", ctypes.c_uint32), ("n_models", ctypes.c_uint32),
+                ("coarse_bits", ctypes.c_uint32), ("warps_per_block", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -162,3 +162,29 @@ def test_large_model_tables_use_narrow_ctas(K, length):
     sym, mid = _draw(rng, models, 300_000, K)
     c = R.recoil_encode_adaptive(sym, mid, models, 16, 64)
     _check(c, mid, sym, oracle_check=True)
+
+
+# K = 64 models of E / 64 entries each (all f > 0): the table sizes force each coarse-bucket
+# choice of the plan (2^9, 2^8, 2^7 buckets on the 32-warp kernel; 2^6 on the 8-warp one).
+CBITS_CASES = [(5000, 9, 32), (12000, 8, 32), (18000, 7, 32), (24000, 6, 8)]
+
+
+def _cbits_models(E, K=64, seed=0):
+    rng = np.random.default_rng(seed + E)
+    length = E // K
+    fs = [oracle.quantize(rng.integers(1, 1000, size=length).astype(np.uint64), 16) for _ in range(K)]
+    return {"base": np.arange(K, dtype=np.uint32) * 700, "len": np.full(K, length, np.uint32),
+            "f": np.concatenate(fs)}
+
+
+@pytest.mark.parametrize("E,cbits,warps", CBITS_CASES)
+def test_coarse_bits_choice_each_geometry(E, cbits, warps):
+    models = _cbits_models(E)
+    rng = np.random.default_rng(E)
+    sym, mid = _draw(rng, models, 400_000, 64)
+    c = R.recoil_encode_adaptive(sym, mid, models, 16, 300)
+    rc, bad, out, plan = gpu_decode_adaptive(c, mid)
+    assert (plan["coarse_bits"], plan["warps_per_block"]) == (cbits, warps)
+    assert rc == 0 and (out == sym).all()
+    w, _ = R.recoil_decode_occupancy_adaptive(0, 64, E)
+    assert (w == 32) == (warps == 32)  # the occupancy query (trimmed entry count) agrees with the plan

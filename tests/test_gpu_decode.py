@@ -434,3 +434,92 @@ def test_config5_8GiB_full_size_sharded():
     for t in (0, M // 3, M - 2, M - 1):
         want, lo, hi = oracle.recoil_decode_task(c.tobytes(), int(t), full)
         assert np.array_equal(want[lo:hi + 1], sym[lo:hi + 1]), t
+
+
+class _Bits:
+    """MSB-first bit reader / writer over the container's global series (test helper)."""
+
+    def __init__(self, data=b"", pos=0):
+        self.bits = "".join(f"{b:08b}" for b in data)
+        self.pos = pos
+
+    def get(self, n):
+        v = int(self.bits[self.pos:self.pos + n], 2)
+        self.pos += n
+        return v
+
+    def series(self, count):  # signed, 5-bit width field (w - 1), magnitude then sign bit
+        w = self.get(5) + 1
+        out = []
+        for _ in range(count):
+            m = self.get(w)
+            out.append(-m if self.get(1) else m)
+        return out
+
+
+def _put_series(vals):
+    w = max(1, max(abs(v).bit_length() for v in vals))
+    bits = f"{w - 1:05b}" + "".join(f"{abs(v):0{w}b}" + ("1" if v < 0 else "0") for v in vals)
+    return bits
+
+
+def _move_max_group(c, k, delta):
+    """Re-serialise a Recoil container with split point k's max group moved by delta groups
+    (header 28 B, model block, 32 u32 finals, two signed series, byte padded)."""
+    raw = bytes(c)
+    count = raw[28] | raw[29] << 8
+    g0 = 28 + 2 + 5 * count + 4 * 32
+    P = R.recoil_inspect(c)["n_splits"] - 1
+    br = _Bits(raw[g0:])
+    doff, dg = br.series(P), br.series(P)
+    end = g0 + (br.pos + 7) // 8
+    dg[k] += delta
+    bits = _put_series(doff) + _put_series(dg)
+    bits += "0" * (-len(bits) % 8)
+    glob = bytes(int(bits[i:i + 8], 2) for i in range(0, len(bits), 8))
+    return np.frombuffer(raw[:g0] + glob + raw[end:], dtype=np.uint8).copy()
+
+
+def test_crafted_record_cannot_write_outside_the_plan():
+    """a middle split point whose max group is moved 2000 groups up (still
+    < G, so the light parse accepts it) must not make its task write past the plan's output
+    window: the kernel checks every task's window against [out_base, out_base + out_count)
+    and flags E_INCONSISTENT.  Guard bytes on both sides of d_out stay untouched."""
+    sym = synth.exp_bytes(2_000_000, 50, 4)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 512)
+    assert bytes(_move_max_group(c, 105, 0)) == bytes(c)  # the re-serialiser is exact
+    bad = _move_max_group(c, 105, 2000)  # point 105 = the entry of task 105, inside the plan [100, 110)
+    dec = R.GpuDecoder(bad, 0, 100, 110)
+    guard = 1 << 20
+    assert 2000 * 32 < guard
+    big = torch.full((dec.plan["out_count"] + 2 * guard,), 0xAB, dtype=torch.uint8, device="cuda")
+    dec.upload()
+    dec.decode(out=big[guard:guard + dec.plan["out_count"]])
+    rc, _ = dec.status()
+    dec.close()
+    assert R.ERRORS.get(rc) == "RECOIL_E_INCONSISTENT"
+    host = big.cpu().numpy()
+    assert (host[:guard] == 0xAB).all() and (host[-guard:] == 0xAB).all()
+
+
+@pytest.mark.timeout(900)
+def test_one_task_longer_than_2pow31_symbols():
+    """One task spanning more than 2^31 symbols (decoder-side combine to one split of a
+    2^31 + 2^21 + 777-symbol stream): the per-task block offsets are unsigned 32-bit and
+    the decode is bit-exact (was silently skipped with signed offsets)."""
+    N = (1 << 31) + (1 << 21) + 777
+    sym = synth.image_bytes(N, synth.seed_for(5, 32))
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 64)
+    for target in (1, 2):
+        dec = R.GpuDecoder(c, 0, subset=target)
+        dec.upload()
+        dec.decode()
+        rc, bad = dec.status()
+        assert rc == 0, (R.ERRORS.get(rc), bad)
+        assert dec.plan["n_tasks"] == target
+        out = dec.output().cpu().numpy()
+        dec.close()
+        assert np.array_equal(out, sym)
+        del out

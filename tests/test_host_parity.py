@@ -373,3 +373,21 @@ def test_grouped_plans():
             R.recoil_decoder_create_grouped(c, *bad)
     with pytest.raises(R.RecoilError):
         R.recoil_decoder_create_grouped(R.recoil_partitioned_encode(sym, f, 11, 8), [2], [2])
+
+
+@pytest.mark.parametrize("E,cbits,warps", [(5000, 9, 32), (12000, 8, 32), (18000, 7, 32), (24000, 6, 8)])
+def test_adaptive_plan_coarse_bits(E, cbits, warps):
+    """The host plan picks the most coarse-bucket bits (9..7) whose tables fit beside the
+    32-warp layout in one block's shared memory, else 6 bits on 8-warp CTAs (no GPU needed)."""
+    K, length = 64, E // 64
+    rng = np.random.default_rng(E)
+    fs = [R.recoil_quantize(rng.integers(1, 1000, size=length).astype(np.uint64), 16) for _ in range(K)]
+    models = {"base": np.arange(K, dtype=np.uint32) * 700, "len": np.full(K, length, np.uint32),
+              "f": np.concatenate(fs)}
+    mid = rng.integers(0, K, size=5000).astype(np.uint8)
+    sym = (models["base"][mid] + rng.integers(0, length, size=5000)).astype(np.uint16)
+    c = R.recoil_encode_adaptive(sym, mid, models, 16, 4)
+    h = R.recoil_decoder_create(c)
+    plan = R.recoil_decoder_plan(h)
+    R.recoil_decoder_destroy(h)
+    assert (plan["coarse_bits"], plan["warps_per_block"]) == (cbits, warps)
