@@ -9,9 +9,11 @@
 // is the oldest entry of an LRU list of the lanes' last events, and candidate
 // windows are evaluated from a bounded event buffer.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <deque>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../recoil_internal.h"
@@ -350,20 +352,34 @@ int encode_partitioned(const uint8_t *sym, uint64_t N, const uint32_t freqs[256]
     return RECOIL_OK;
   }
   uint64_t G = ceil_div(N, kLanes);
-  std::vector<uint16_t> words, part;
+  // partitions are independent codecs: encode them on several threads,
+  // each into its own word vector, then concatenate in partition order
+  std::vector<std::vector<uint16_t>> parts(P);
   std::vector<uint32_t> cnt(P), fin((size_t)P * kLanes);
-  words.reserve(N / 2 + 64);
+  std::vector<int> prc(P, RECOIL_OK);
+  std::atomic<uint64_t> next{0};
+  auto worker = [&]() {
+    for (uint64_t p; (p = next.fetch_add(1)) < P;) {
+      uint64_t lo = kLanes * (p * G / P), hi = std::min<uint64_t>(N, kLanes * ((p + 1) * G / P));
+      if (lo > hi) lo = hi;
+      parts[p].reserve((hi - lo) / 2 + 64);
+      prc[p] = interleaved_encode<false>(sym + lo, hi - lo, si, n, &parts[p], &fin[p * kLanes], nullptr);
+      if (!prc[p] && (parts[p].size() >> 32)) prc[p] = RECOIL_E_OVERFLOW;
+    }
+  };
+  const uint32_t nt = (uint32_t)std::min<uint64_t>({P, (uint64_t)std::max(1u, std::thread::hardware_concurrency()),
+                                                    std::max<uint64_t>(1, N >> 22)});
+  std::vector<std::thread> pool;
+  for (uint32_t i = 1; i < nt; ++i) pool.emplace_back(worker);
+  worker();
+  for (auto &th : pool) th.join();
+  uint64_t n_words = 0;
   for (uint64_t p = 0; p < P; ++p) {
-    uint64_t lo = kLanes * (p * G / P), hi = std::min<uint64_t>(N, kLanes * ((p + 1) * G / P));
-    if (lo > hi) lo = hi;
-    part.clear();
-    rc = interleaved_encode<false>(sym + lo, hi - lo, si, n, &part, &fin[p * kLanes], nullptr);
-    if (rc) return rc;
-    if (part.size() >> 32) return RECOIL_E_OVERFLOW;
-    cnt[p] = (uint32_t)part.size();
-    words.insert(words.end(), part.begin(), part.end());
+    if (prc[p]) return prc[p];
+    cnt[p] = (uint32_t)parts[p].size();
+    n_words += parts[p].size();
   }
-  uint64_t total = fixed + 2 * words.size();
+  uint64_t total = fixed + 2 * n_words;
   if (*len < total) {
     *len = total;
     return RECOIL_E_BUFFER;
@@ -376,7 +392,7 @@ int encode_partitioned(const uint8_t *sym, uint64_t N, const uint32_t freqs[256]
   q[7] = (uint8_t)kLanes;
   put_le(q + 8, P, 4);
   put_le(q + 12, N, 8);
-  put_le(q + 20, words.size(), 8);
+  put_le(q + 20, n_words, 8);
   q += 28;
   put_le(q, count, 2);
   q += 2;
@@ -388,7 +404,8 @@ int encode_partitioned(const uint8_t *sym, uint64_t N, const uint32_t freqs[256]
     }
   for (uint64_t p = 0; p < P; ++p, q += 4) put_le(q, cnt[p], 4);
   for (size_t k = 0; k < fin.size(); ++k, q += 4) put_le(q, fin[k], 4);
-  for (size_t w = 0; w < words.size(); ++w, q += 2) put_le(q, words[w], 2);
+  for (uint64_t p = 0; p < P; ++p)  // u16 little endian (host is little endian, as the container)
+    for (size_t w = 0; w < parts[p].size(); ++w, q += 2) put_le(q, parts[p][w], 2);
   *len = total;
   return RECOIL_OK;
 }

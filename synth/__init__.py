@@ -53,6 +53,8 @@ def _load():
                                           ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_int]
         lib.synth_fill_models.restype = ctypes.c_int
+        lib.synth_histogram.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
+        lib.synth_histogram.restype = None
         _lib = lib
     return _lib
 
@@ -172,10 +174,10 @@ def workload(kind: str, n: int, seed: int, lam: float = 50.0) -> np.ndarray:
 
 
 def histogram(sym: np.ndarray) -> np.ndarray:
-    # chunked: np.bincount widens its input to intp (8 bytes per symbol at once otherwise)
+    """Byte histogram (256 x u64) of a uint8 array, multithreaded in synth.c."""
+    sym = np.ascontiguousarray(sym, dtype=np.uint8)
     h = np.zeros(256, np.uint64)
-    for i in range(0, len(sym), 1 << 26):
-        h += np.bincount(sym[i:i + (1 << 26)], minlength=256).astype(np.uint64)
+    _load().synth_histogram(sym.ctypes.data, len(sym), h.ctypes.data, max(1, min(16, os.cpu_count() or 1)))
     return h
 
 

@@ -141,3 +141,47 @@ int synth_fill_models(uint16_t *out, const uint8_t *mid, uint64_t start, uint64_
   for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
   return 0;
 }
+
+/* Byte histogram of x[0..n) (input statistics for the model the tests and the
+ * bench build; no method arithmetic), on up to `threads` threads. */
+typedef struct {
+  const uint8_t *x;
+  uint64_t n;
+  uint64_t h[256];
+} hjob_t;
+
+static void *run_hjob(void *arg) {
+  hjob_t *j = (hjob_t *)arg;
+  uint64_t h4[4][256] = {{0}};
+  uint64_t i = 0;
+  for (; i + 4 <= j->n; i += 4) {
+    ++h4[0][j->x[i]];
+    ++h4[1][j->x[i + 1]];
+    ++h4[2][j->x[i + 2]];
+    ++h4[3][j->x[i + 3]];
+  }
+  for (; i < j->n; ++i) ++h4[0][j->x[i]];
+  for (int k = 0; k < 256; ++k) j->h[k] = h4[0][k] + h4[1][k] + h4[2][k] + h4[3][k];
+  return NULL;
+}
+
+void synth_histogram(const uint8_t *x, uint64_t n, uint64_t *hist, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  if (n < (1u << 22)) threads = 1;
+  pthread_t th[64];
+  hjob_t jobs[64];
+  for (int t = 0; t < threads; ++t) {
+    uint64_t b = n * (uint64_t)t / (uint64_t)threads, e = n * (uint64_t)(t + 1) / (uint64_t)threads;
+    jobs[t].x = x + b;
+    jobs[t].n = e - b;
+  }
+  for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, run_hjob, &jobs[t]);
+  run_hjob(&jobs[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  for (int k = 0; k < 256; ++k) {
+    uint64_t s = 0;
+    for (int t = 0; t < threads; ++t) s += jobs[t].h[k];
+    hist[k] = s;
+  }
+}
