@@ -279,6 +279,16 @@ int recoil_pipeline_device_bytes(const recoil_pipeline *p, uint32_t n_streams, u
 int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t *host_out, void *const *streams,
                         uint32_t n_streams);
 
+/* recoil_pipeline_run with host_out indexed from symbol host_first instead of 0:
+ * the chunk symbols [out_lo, out_hi) go to host_out[out_lo - host_first, ...),
+ * so a shard's caller needs only a buffer of its own span (host_first = the
+ * span's out_lo from recoil_pipeline_span).  E_ARG if host_first > out_lo. */
+int recoil_pipeline_run_at(recoil_pipeline *p, void *d_scratch, uint8_t *host_out, uint64_t host_first,
+                           void *const *streams, uint32_t n_streams);
+
+/* Committed symbols [*out_lo, *out_hi) of the pipeline's task range. */
+int recoil_pipeline_span(const recoil_pipeline *p, uint64_t *out_lo, uint64_t *out_hi);
+
 /* Synchronise the streams and fold the chunks' status words (as
  * recoil_decoder_status).  *bad_task (may be NULL): first failing task. */
 int recoil_pipeline_status(recoil_pipeline *p, void *const *streams, uint32_t n_streams, uint64_t *bad_task);
@@ -297,6 +307,37 @@ void recoil_pipeline_destroy(recoil_pipeline *p);
  * task_bounds: n_shards + 1 entries, task_bounds[0] = 0,
  * task_bounds[n_shards] = M.  Errors: E_ARG, container errors. */
 int recoil_shard_plan(const uint8_t *container, uint64_t len, uint32_t n_shards, uint64_t *task_bounds);
+
+/* Single-process multi-GPU decode (the split tasks
+ * are "completely independent" and "can be scaled over multiple cores").
+ * recoil_multi_plan: the decode plan of each of n_dev shards (recoil_shard_plan
+ * ranges); plans[d].out_count symbols is the size of d_outs[d], laid out as for
+ * recoil_decode (d_outs[d][i - plans[d].out_base]).  plans: n_dev entries.
+ * Errors: container errors, E_ARG, E_NOMEM, E_UNSUPPORTED (adaptive container:
+ * it needs per-symbol model ids, use recoil_decode_adaptive per device). */
+int recoil_multi_plan(const uint8_t *container, uint64_t len, uint32_t n_dev, recoil_plan *plans);
+
+/* Decode shard d on CUDA device devices[d] into the caller's device buffer
+ * d_outs[d] (on that device, plans[d].out_count bytes).  Each device gets its
+ * own stream, workspace and word slice (allocated stream-ordered from that
+ * device's pool, freed before return); all devices are enqueued before any is
+ * waited on, so distinct GPUs decode concurrently.  Synchronous: returns after
+ * every device finished.  gather_root >= 0: afterwards every shard's committed
+ * span [out_lo, out_hi) is copied into d_gather[out_lo, out_hi) on
+ * devices[gather_root] (d_gather: N bytes on that device) -- one NCCL group of
+ * ncclSend/ncclRecv (libnccl.so.2, loaded at run time) when the devices are
+ * distinct, else (shards sharing a GPU, or no NCCL) cudaMemcpyPeerAsync; the
+ * gather is skipped when a decode failed.  gather_root = -1: no gather.
+ * kernel_ms (may be NULL): n_dev decode-kernel times (CUDA events per device).
+ * Returns the most severe device status (E_INCONSISTENT, E_UNSUPPORTED,
+ * E_UNDERFLOW, E_SYNC) or RECOIL_OK.  The current device is restored.
+ * Errors: as recoil_multi_plan, E_ARG (NULL d_outs[d] of a shard with tasks,
+ * gather_root >= n_dev, gather without d_gather), E_CUDA. */
+int recoil_multi_decode(const uint8_t *container, uint64_t len, uint32_t n_dev, const int *devices,
+                        uint8_t *const *d_outs, int gather_root, uint8_t *d_gather, float *kernel_ms);
+
+/* 1 if recoil_multi_decode can gather over NCCL (libnccl.so.2 loadable), else 0. */
+int recoil_multi_nccl_available(void);
 
 /* ---------------------------------------------------------------------- */
 /* Host baselines (NOT a fallback of the GPU path: separate entry points)  */

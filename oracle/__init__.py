@@ -82,6 +82,9 @@ def _load():
         "or_recoil_decode": (i32, [P, u64, P]),
         "or_recoil_decode_task": (i32, [P, u64, u32, P, P, P]),
         "or_recoil_decode_tasks": (i32, [P, u64, P, u32, P, P]),
+        "or_open": (i32, [P, u64, P]),
+        "or_opened_decode_tasks": (i32, [P, P, u32, P, P]),
+        "or_close": (None, [P]),
         "or_partitioned_encode": (i32, [P, u64, P, u32, u32, u32, P, P]),
         "or_partitioned_decode": (i32, [P, u64, P]),
         "or_quantize": (i32, [P, u32, u32, P]),
@@ -306,6 +309,34 @@ def recoil_decode_tasks(container: bytes, tasks, out: np.ndarray | None = None):
     n = ctypes.c_uint64(0)
     _check(_load().or_recoil_decode_tasks(c.ctypes.data, c.size, _ptr(t), t.size, out.ctypes.data, ctypes.byref(n)))
     return out, n.value
+
+
+class Opened:
+    """A container parsed once (or_open) for repeated task decodes; the parse stays
+    outside any timed region that uses decode_tasks."""
+
+    def __init__(self, container: bytes):
+        self._c = _u8(container)  # or_open keeps pointers into the container bytes
+        self.info = container_info(container)
+        self.h = ctypes.c_void_p()
+        _check(_load().or_open(self._c.ctypes.data, self._c.size, ctypes.byref(self.h)))
+
+    def decode_tasks(self, tasks, out: np.ndarray):
+        t = np.ascontiguousarray(np.asarray(tasks, dtype=np.uint32))
+        n = ctypes.c_uint64(0)
+        _check(_load().or_opened_decode_tasks(self.h, _ptr(t), t.size, out.ctypes.data, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.h:
+            _load().or_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def partitioned_encode(sym, f, n: int, P: int, W: int = 32) -> bytes:

@@ -895,6 +895,45 @@ int or_recoil_decode_tasks(const uint8_t *c, uint64_t len, const uint32_t *tasks
   return rc;
 }
 
+/* A container parsed once (box_read + box_words) for repeated task decodes:
+ * the reference arm times or_opened_decode_tasks only, with the parse outside
+ * its timed region. */
+struct or_opened {
+  or_box bx;
+  uint16_t *w;
+};
+
+int or_open(const uint8_t *c, uint64_t len, or_opened **out) {
+  or_opened *h = (or_opened *)calloc(1, sizeof(or_opened));
+  if (!h) return OR_E_ARG;
+  int rc = box_read(c, len, &h->bx);
+  if (rc) { free(h); return rc; }
+  h->w = box_words(&h->bx);
+  *out = h;
+  return OR_OK;
+}
+
+int or_opened_decode_tasks(or_opened *h, const uint32_t *tasks, uint32_t n_tasks, uint8_t *out,
+                           uint64_t *n_symbols) {
+  int rc = OR_OK;
+  uint64_t total = 0;
+  for (uint32_t k = 0; k < n_tasks && rc == OR_OK; ++k) {
+    uint64_t lo = 0, hi = 0;
+    if (tasks[k] >= h->bx.M || h->bx.N == 0) { rc = OR_E_ARG; break; }
+    rc = box_task(&h->bx, h->w, tasks[k], out, &lo, &hi);
+    total += hi - lo + 1;
+  }
+  if (n_symbols) *n_symbols = total;
+  return rc;
+}
+
+void or_close(or_opened *h) {
+  if (!h) return;
+  free(h->w);
+  box_free(&h->bx);
+  free(h);
+}
+
 int or_recoil_decode_task(const uint8_t *c, uint64_t len, uint32_t task, uint8_t *out,
                           uint64_t *lo, uint64_t *hi) {
   or_box bx;

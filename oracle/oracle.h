@@ -94,6 +94,12 @@ int or_container_info(const uint8_t *c, uint64_t len, uint64_t info[8]);
 int or_container_points(const uint8_t *c, uint64_t len, uint64_t *offset, uint64_t *maxg,
                         uint64_t *sync_start, uint64_t *bidx);
 int or_recoil_decode(const uint8_t *c, uint64_t len, uint8_t *out);
+/* A container parsed once for repeated task decodes (bounded CPU samples). */
+typedef struct or_opened or_opened;
+int or_open(const uint8_t *c, uint64_t len, or_opened **out);
+int or_opened_decode_tasks(or_opened *h, const uint32_t *tasks, uint32_t n_tasks, uint8_t *out,
+                           uint64_t *n_symbols);
+void or_close(or_opened *h);
 int or_recoil_decode_task(const uint8_t *c, uint64_t len, uint32_t task, uint8_t *out,
                           uint64_t *lo, uint64_t *hi);
 int or_recoil_decode_tasks(const uint8_t *c, uint64_t len, const uint32_t *tasks, uint32_t n_tasks,

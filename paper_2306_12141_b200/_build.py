@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(res.stderr)
         objs.append(obj)
     if force or _stale(LIB, objs):
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-ldl"])
     return LIB
 
 

@@ -42,6 +42,7 @@ struct Pipeline {
   std::vector<Decoder> dec;        // the last run's chunk plans (alive until status)
   int single_symbol = -1;
   uint32_t prev_streams = 0;       // buffer sets the previous run used (its work may still be queued)
+  uint64_t out_lo = 0, out_hi = 0; // committed symbols of the task range
 
   ~Pipeline() {
     for (auto &p : staging)
@@ -91,7 +92,11 @@ extern "C" int recoil_pipeline_create(const uint8_t *container, uint64_t len, ui
       delete pl;
       return rc;
     }
+    pl->out_lo = pl->dec.front().plan.out_lo;
+    pl->out_hi = pl->dec.back().plan.out_hi;
     for (const Decoder &d : pl->dec) {
+      pl->out_lo = std::min(pl->out_lo, d.plan.out_lo);
+      pl->out_hi = std::max(pl->out_hi, d.plan.out_hi);
       pl->ws_bytes = std::max(pl->ws_bytes, align256(d.plan.workspace_bytes));
       pl->word_bytes = std::max(pl->word_bytes, align256(2 * d.plan.word_count));
       pl->out_bytes = std::max(pl->out_bytes, align256(d.plan.out_count));
@@ -117,11 +122,25 @@ extern "C" int recoil_pipeline_device_bytes(const recoil_pipeline *p, uint32_t n
   return RECOIL_OK;
 }
 
+extern "C" int recoil_pipeline_span(const recoil_pipeline *p, uint64_t *out_lo, uint64_t *out_hi) {
+  if (!p || !out_lo || !out_hi) return RECOIL_E_ARG;
+  const Pipeline *pl = reinterpret_cast<const Pipeline *>(p);
+  *out_lo = pl->out_lo;
+  *out_hi = pl->out_hi;
+  return RECOIL_OK;
+}
+
 extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t *host_out, void *const *streams,
                                    uint32_t n_streams) {
+  return recoil_pipeline_run_at(p, d_scratch, host_out, 0, streams, n_streams);
+}
+
+extern "C" int recoil_pipeline_run_at(recoil_pipeline *p, void *d_scratch, uint8_t *host_out, uint64_t host_first,
+                                      void *const *streams, uint32_t n_streams) {
   if (!p || !d_scratch || !streams || n_streams < 1 || n_streams > kMaxStreams) return RECOIL_E_ARG;
   Pipeline *pl = reinterpret_cast<Pipeline *>(p);
   if (pl->N && !host_out) return RECOIL_E_ARG;
+  if (pl->out_hi > pl->out_lo && host_first > pl->out_lo) return RECOIL_E_ARG;
   try {
     // a previous run enqueued without an intervening status call may still be
     // reading its buffer sets, staging and status words: wait for its last D2H per
@@ -197,7 +216,7 @@ extern "C" int recoil_pipeline_run(recoil_pipeline *p, void *d_scratch, uint8_t 
       if (cudaEventRecord(pl->ev_k[s], sc) != cudaSuccess || cudaStreamWaitEvent(so, pl->ev_k[s], 0) != cudaSuccess)
         return RECOIL_E_CUDA;
       if (pn.out_hi > pn.out_lo &&
-          cudaMemcpyAsync(host_out + pn.out_lo, dout + (pn.out_lo - pn.out_base), pn.out_hi - pn.out_lo,
+          cudaMemcpyAsync(host_out + (pn.out_lo - host_first), dout + (pn.out_lo - pn.out_base), pn.out_hi - pn.out_lo,
                           cudaMemcpyDeviceToHost, so) != cudaSuccess)
         return RECOIL_E_CUDA;
       if (cudaMemcpyAsync(&pl->status[k], ws, sizeof(DeviceStatus), cudaMemcpyDeviceToHost, so) != cudaSuccess ||

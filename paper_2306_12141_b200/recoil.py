@@ -35,7 +35,8 @@ EXPORTS = [
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
     "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
     "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive", "recoil_decoder_create_subset",
-    "recoil_decoder_create_grouped",
+    "recoil_decoder_create_grouped", "recoil_pipeline_run_at", "recoil_pipeline_span", "recoil_multi_plan",
+    "recoil_multi_decode", "recoil_multi_nccl_available",
 ]
 
 
@@ -109,6 +110,11 @@ def load(path: str = LIB_PATH):
         "recoil_decode_occupancy_adaptive": (i32, [i32, u32, u64, P, P]),
         "recoil_decoder_create_subset": (i32, [P, u64, u32, u64, u64, P]),
         "recoil_decoder_create_grouped": (i32, [P, u64, u32, P, P, P]),
+        "recoil_pipeline_run_at": (i32, [P, P, P, u64, P, u32]),
+        "recoil_pipeline_span": (i32, [P, P, P]),
+        "recoil_multi_plan": (i32, [P, u64, u32, P]),
+        "recoil_multi_decode": (i32, [P, u64, u32, P, P, i32, P, P]),
+        "recoil_multi_nccl_available": (i32, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -421,6 +427,17 @@ def recoil_pipeline_run(handle, d_scratch: int, host_out: int, streams) -> None:
     _check(load().recoil_pipeline_run(handle, d_scratch, host_out, arr, n), "recoil_pipeline_run")
 
 
+def recoil_pipeline_run_at(handle, d_scratch: int, host_out: int, host_first: int, streams) -> None:
+    arr, n = _streams(streams)
+    _check(load().recoil_pipeline_run_at(handle, d_scratch, host_out, host_first, arr, n), "recoil_pipeline_run_at")
+
+
+def recoil_pipeline_span(handle) -> tuple[int, int]:
+    lo, hi = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(load().recoil_pipeline_span(handle, ctypes.byref(lo), ctypes.byref(hi)), "recoil_pipeline_span")
+    return lo.value, hi.value
+
+
 def recoil_pipeline_status(handle, streams) -> tuple[int, int | None]:
     arr, n = _streams(streams)
     bad = ctypes.c_uint64(0)
@@ -451,9 +468,15 @@ class HostPipeline:
         self.scratch = torch.empty(max(recoil_pipeline_device_bytes(self.handle, n_streams), 256),
                                    dtype=torch.uint8, device=self.device)
 
-    def run(self, host_out) -> None:
+    def run(self, host_out, host_first: int = 0) -> None:
+        """host_out[i - host_first] receives symbol i of the pipeline's span (host_first = 0:
+        a buffer of the whole stream; = span()[0]: a buffer of the span only)."""
         ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
-        recoil_pipeline_run(self.handle, self.scratch.data_ptr(), ptr, [s.cuda_stream for s in self.streams])
+        recoil_pipeline_run_at(self.handle, self.scratch.data_ptr(), ptr, host_first,
+                               [s.cuda_stream for s in self.streams])
+
+    def span(self) -> tuple[int, int]:
+        return recoil_pipeline_span(self.handle)
 
     def status(self):
         return recoil_pipeline_status(self.handle, [s.cuda_stream for s in self.streams])
@@ -488,6 +511,34 @@ def decode_gpu(container, device: int = 0):
 
 
 # --- multi-GPU (§8(e), row a10): optional gather of the shards' spans ----------------------
+
+def recoil_multi_plan(container, n_dev: int) -> list[dict]:
+    c = _u8(container)
+    plans = (recoil_plan * n_dev)()
+    _check(load().recoil_multi_plan(c.ctypes.data, c.size, n_dev, plans), "recoil_multi_plan")
+    return [p.as_dict() for p in plans]
+
+
+def recoil_multi_nccl_available() -> bool:
+    return bool(load().recoil_multi_nccl_available())
+
+
+def recoil_multi_decode(container, devices, d_outs, gather_root: int = -1, d_gather=None):
+    """Single-process multi-GPU decode through the C ABI: shard d on CUDA device
+    devices[d] into the torch tensor d_outs[d] (plans[d]["out_count"] bytes on that
+    device); optional gather of every committed span into d_gather (N bytes on
+    devices[gather_root]).  Returns (status, per-device kernel ms)."""
+    c = _u8(container)
+    n = len(devices)
+    devs = (ctypes.c_int * n)(*devices)
+    outs = (ctypes.c_void_p * n)(*[o.data_ptr() if o is not None else None for o in d_outs])
+    ms = (ctypes.c_float * n)()
+    rc = load().recoil_multi_decode(c.ctypes.data, c.size, n, devs, outs, gather_root,
+                                    d_gather.data_ptr() if d_gather is not None else None, ms)
+    if rc in (RECOIL_E_ARG, RECOIL_E_CUDA, RECOIL_E_NOMEM) or rc <= RECOIL_E_BAD_MAGIC and rc >= RECOIL_E_TRUNCATED:
+        raise RecoilError(rc, "recoil_multi_decode")
+    return rc, list(ms)
+
 
 def shard_spans(container, world: int) -> list[tuple[int, int, int, int]]:
     """(task_begin, task_end, out_lo, out_hi) of every rank's shard of `container`

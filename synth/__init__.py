@@ -132,17 +132,17 @@ def _fill(n: int, seed: int, tables: np.ndarray, tile: int = 0, start: int = 0, 
     return out
 
 
-def exp_bytes(n: int, lam: float, seed: int) -> np.ndarray:
-    return _fill(n, seed, _tables_array([exp_pmf(lam)]))
+def exp_bytes(n: int, lam: float, seed: int, start: int = 0) -> np.ndarray:
+    return _fill(n, seed, _tables_array([exp_pmf(lam)]), start=start)
 
 
-def text_bytes(n: int, seed: int, s: float = 1.0574) -> np.ndarray:
-    return _fill(n, seed, _tables_array([text_pmf(s)]))
+def text_bytes(n: int, seed: int, s: float = 1.0574, start: int = 0) -> np.ndarray:
+    return _fill(n, seed, _tables_array([text_pmf(s)]), start=start)
 
 
-def image_bytes(n: int, seed: int) -> np.ndarray:
+def image_bytes(n: int, seed: int, start: int = 0) -> np.ndarray:
     levels = [0.15 * (20.0 ** (l / (IMAGE_LEVELS - 1))) for l in range(IMAGE_LEVELS)]
-    return _fill(n, seed, _tables_array([laplace_residual_pmf(b) for b in levels]), tile=IMAGE_TILE)
+    return _fill(n, seed, _tables_array([laplace_residual_pmf(b) for b in levels]), tile=IMAGE_TILE, start=start)
 
 
 def table_bytes(n: int, pmf, seed: int) -> np.ndarray:
@@ -163,13 +163,15 @@ def seed_for(config_id: int, lam: float = 0) -> int:
     return 0x5EC011 + config_id * 1000 + int(lam)
 
 
-def workload(kind: str, n: int, seed: int, lam: float = 50.0) -> np.ndarray:
+def workload(kind: str, n: int, seed: int, lam: float = 50.0, start: int = 0) -> np.ndarray:
+    """Symbols [start, start + n) of the seeded stream (any sub-range is generated
+    independently: the draws are counter-based)."""
     if kind == "exp":
-        return exp_bytes(n, lam, seed)
+        return exp_bytes(n, lam, seed, start)
     if kind == "text":
-        return text_bytes(n, seed)
+        return text_bytes(n, seed, start=start)
     if kind == "image":
-        return image_bytes(n, seed)
+        return image_bytes(n, seed, start)
     raise ValueError(kind)
 
 

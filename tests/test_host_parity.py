@@ -391,3 +391,27 @@ def test_adaptive_plan_coarse_bits(E, cbits, warps):
     plan = R.recoil_decoder_plan(h)
     R.recoil_decoder_destroy(h)
     assert (plan["coarse_bits"], plan["warps_per_block"]) == (cbits, warps)
+
+
+def test_multi_plan_equals_shard_plan_and_decoder_plans():
+    """recoil_multi_plan (C ABI multi-GPU entry, §8(b)) = recoil_shard_plan's ranges with
+    each range's decoder plan; the spans tile [0, N)."""
+    import synth
+    from paper_2306_12141_b200 import recoil as R
+    sym = synth.workload("text", 500_000, seed=7)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 120)
+    for n_dev in (1, 2, 5, 8):
+        plans = R.recoil_multi_plan(c, n_dev)
+        bounds = R.recoil_shard_plan(c, n_dev)
+        lo = 0
+        for d, p in enumerate(plans):
+            h = R.recoil_decoder_create(c, bounds[d], bounds[d + 1])
+            want = R.recoil_decoder_plan(h)
+            R.recoil_decoder_destroy(h)
+            assert p == want
+            assert p["out_lo"] == lo
+            lo = p["out_hi"]
+        assert lo == len(sym)
+    with pytest.raises(R.RecoilError):
+        R.recoil_multi_plan(c, 0)
