@@ -640,19 +640,18 @@ def main():
                          f"{dt:.1f} s); container parsed once ({open_s:.1f} s, untimed)",
                "bit_exact": cok, "cpu": cpuinfo}
         threads = cpuinfo["physical_cores"]  # one thread per physical core, no SMT
-        for key, flags, note in (("cpu_mt_library", R.RECOIL_CPU_SCALAR, "recoil_decode_cpu_ex(SCALAR): scalar MT "
-                                  "host decoder (baseline, not a fallback)"),
-                                 ("cpu_mt_simd", 0, "recoil_decode_cpu: SIMD MT host decoder (NEXT row 3; "
-                                  "baseline)")):
-            if flags == 0 and not R.recoil_cpu_simd():
-                continue
+        legs = [("cpu_mt_library", R.RECOIL_CPU_SCALAR, "recoil_decode_cpu_ex(SCALAR): scalar MT host decoder")]
+        if R.recoil_cpu_simd() >= 1:
+            legs.append(("cpu_mt_avx2", R.RECOIL_CPU_AVX2, "recoil_decode_cpu_ex(AVX2): 8 lanes x 4 vectors"))
+        if R.recoil_cpu_simd() == 2:
+            legs.append(("cpu_mt_avx512", 0, "recoil_decode_cpu: AVX-512, 16 lanes x 2 vectors"))
+        for key, flags, note in legs:
             t0 = time.perf_counter()
             out_cpu = R.recoil_decode_cpu_ex(c, threads, flags)
             dt_mt = time.perf_counter() - t0
             extra[key] = {"value": round(N_total / dt_mt / 1e9, 4), "unit": "GB/s", "threads": threads,
-                          "bit_exact": bool(np.array_equal(out_cpu, sym)), "cpu": cpuinfo, "note": note}
-            if flags == 0:
-                extra[key]["isa"] = R.recoil_cpu_isa() if hasattr(R, "recoil_cpu_isa") else "avx512"
+                          "bit_exact": bool(np.array_equal(out_cpu, sym)), "cpu": cpuinfo,
+                          "note": note + " (NEXT row 3, P:429; a host baseline, not a fallback)"}
             del out_cpu
 
     prof = {}

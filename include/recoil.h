@@ -344,16 +344,20 @@ int recoil_multi_nccl_available(void);
 /* ---------------------------------------------------------------------- */
 
 /* Multithreaded CPU Recoil / partitioned decoder: one task per split, up to
- * `threads` threads (0 = hardware concurrency); AVX-512 task decoder when the
- * CPU has AVX-512 F/BW/VL/VBMI2 (P:429's AVX-512 decoder: 16 lanes per
- * instruction, two vectors per 32-lane group), else scalar.  out: N bytes.
+ * `threads` threads (0 = hardware concurrency; P:429 recommends one per
+ * physical core, no SMT).  Task decoder (P:429's CPU decoders): AVX-512 (16
+ * lanes per instruction, two vectors per 32-lane group) when the CPU has
+ * AVX-512 F/BW/VL/VBMI2, else AVX2 (8 lanes per instruction, four vectors per
+ * group), else scalar.  out: N bytes.
  * Errors: container errors, E_UNDERFLOW, E_SYNC. */
 int recoil_decode_cpu(const uint8_t *container, uint64_t len, uint8_t *out, uint32_t threads);
 
 #define RECOIL_CPU_SCALAR 1u /* recoil_decode_cpu_ex flag: force the scalar task decoder */
+#define RECOIL_CPU_AVX2 2u   /* recoil_decode_cpu_ex flag: force the AVX2 task decoder (E_UNSUPPORTED without AVX2) */
 int recoil_decode_cpu_ex(const uint8_t *container, uint64_t len, uint8_t *out, uint32_t threads, uint32_t flags);
 
-/* 1 if recoil_decode_cpu uses the AVX-512 task decoder on this CPU, else 0. */
+/* The SIMD task decoder recoil_decode_cpu uses on this CPU: 2 = AVX-512,
+ * 1 = AVX2, 0 = none (scalar). */
 int recoil_cpu_simd(void);
 
 #ifdef __cplusplus

@@ -1,12 +1,16 @@
 // cpu_decode.cpp -- multithreaded host decoder (baseline, NOT a fallback of the
 // GPU path): the same task table as the GPU kernel, one task per split, one
 // thread per core (P:429 recommends no SMT).  Decodes Recoil and partitioned
-// containers for any 1 <= n <= 16.  Two task decoders: scalar, and AVX-512
-// (NEXT row 3; the paper's CPU decoders are AVX2 / AVX-512): the 32
-// lanes are two 16 x u32 vectors, the refill of a group is one masked
-// expand-load of the needing lanes' words (ascending lanes take ascending
-// words, i.e. the interleaved decreasing-lane read order of P:168), the symbol
-// lookup is a gather from the LUT.
+// containers for any 1 <= n <= 16.  Three task decoders (NEXT row 3; the
+// paper's CPU decoders are AVX2 8-way x 4 and AVX-512 16-way x 2):
+//  - scalar;
+//  - AVX-512: the 32 lanes are two 16 x u32 vectors, the refill of a group is
+//    one masked expand-load of the needing lanes' words (ascending lanes take
+//    ascending words, i.e. the interleaved decreasing-lane read order of P:168);
+//  - AVX2: four 8 x u32 vectors; per vector one 16-byte load of the words its
+//    needing lanes take (a contiguous run below the cursor) and a permutation
+//    from a 256-entry table indexed by the needing-lane mask;
+// in both SIMD decoders the symbol lookup is a gather from the LUT.
 #include <immintrin.h>
 
 #include <algorithm>
@@ -166,6 +170,117 @@ int decode_task_avx512(const Decoder &d, const Tables &tb, const TaskRec &t, con
   return RECOIL_OK;
 }
 
+// AVX2 refill (P:168 read order): vector v holds lanes 8v..8v+7; the vectors are
+// visited from the highest lanes down, and the c needing lanes of a vector take the
+// c words just below the cursor, ascending lane <- ascending word.
+struct Avx2Perm {
+  alignas(32) uint32_t idx[256][8];  // needing-lane mask -> for each lane, its rank among the needing lanes
+  Avx2Perm() {
+    for (uint32_t m = 0; m < 256; ++m)
+      for (uint32_t j = 0; j < 8; ++j) idx[m][j] = (uint32_t)__builtin_popcount(m & ((1u << j) - 1)) & 7u;
+  }
+};
+const Avx2Perm &avx2_perm() {
+  static const Avx2Perm p;
+  return p;
+}
+
+__attribute__((target("avx2,popcnt"))) inline bool avx2_refill(__m256i x[4], int64_t &cur, const uint16_t *w,
+                                                               const Avx2Perm &pm) {
+  for (int v = 3; v >= 0; --v) {
+    const __m256i need = _mm256_cmpeq_epi32(_mm256_srli_epi32(x[v], 16), _mm256_setzero_si256());  // x < L = 2^16
+    const uint32_t m = (uint32_t)_mm256_movemask_ps(_mm256_castsi256_ps(need));
+    if (!m) continue;
+    const int c = __builtin_popcount(m);
+    if (cur - c + 1 < 0) return false;
+    // words [cur - c + 1, cur - c + 8]: the container copy has 8 words of padding past B
+    const __m256i wv = _mm256_cvtepu16_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(w + (cur - c + 1))));
+    const __m256i pw = _mm256_permutevar8x32_epi32(wv, _mm256_load_si256(reinterpret_cast<const __m256i *>(pm.idx[m])));
+    x[v] = _mm256_blendv_epi8(x[v], _mm256_or_si256(_mm256_slli_epi32(x[v], 16), pw), need);
+    cur -= c;
+  }
+  return true;
+}
+
+__attribute__((target("avx2,popcnt")))
+int decode_task_avx2(const Decoder &d, const Tables &tb, const TaskRec &t, const uint16_t *w, uint8_t *out) {
+  const uint32_t n = d.c->n;
+  const Avx2Perm &pm = avx2_perm();
+  const __m256i vmask = _mm256_set1_epi32((int)((1u << n) - 1)), vL = _mm256_set1_epi32((int)kL);
+  const __m256i v16 = _mm256_set1_epi32(0xFFFF), v12 = _mm256_set1_epi32(0xFFF), vff = _mm256_set1_epi32(0xFF);
+  const __m128i vn = _mm_cvtsi32_si128((int)n);
+  const __m256i order = _mm256_setr_epi32(0, 4, 1, 5, 2, 6, 3, 7);
+  alignas(32) uint32_t st[32];
+  alignas(32) int32_t ig[32];
+  for (uint32_t j = 0; j < kLanes; ++j) {
+    st[j] = t.finals_idx == kNoFinals ? (t.lanes[j] & 0xFFFF) : d.finals[t.finals_idx * kLanes + j];
+    ig[j] = t.start_group - (int32_t)(t.lanes[j] >> 16);
+  }
+  __m256i x[4], stv[4], igv[4], in[4];
+  for (int v = 0; v < 4; ++v) {
+    stv[v] = _mm256_load_si256(reinterpret_cast<const __m256i *>(st + 8 * v));
+    igv[v] = _mm256_load_si256(reinterpret_cast<const __m256i *>(ig + 8 * v));
+    x[v] = _mm256_set1_epi32(-1);  // uninitialised lanes: never < L
+    in[v] = _mm256_setzero_si256();
+  }
+  int64_t cur = t.cursor0;
+  const int64_t lo_group = (int64_t)(t.commit_lo / kLanes);
+  const uint64_t out_base = d.plan.out_base;
+  for (int64_t g = t.start_group; g >= lo_group; --g) {
+    const __m256i gv = _mm256_set1_epi32((int)g);
+    for (int v = 0; v < 4; ++v) {
+      const __m256i now = _mm256_cmpeq_epi32(igv[v], gv);
+      x[v] = _mm256_blendv_epi8(x[v], stv[v], now);
+      in[v] = _mm256_or_si256(in[v], now);
+    }
+    if (!avx2_refill(x, cur, w, pm)) return RECOIL_E_UNDERFLOW;
+    __m256i sym[4];
+    for (int v = 0; v < 4; ++v) {
+      const __m256i slot = _mm256_and_si256(x[v], vmask);
+      const __m256i e = _mm256_i32gather_epi32(reinterpret_cast<const int *>(tb.fb.data()), slot, 4);
+      __m256i y;
+      if (n <= 12) {  // packed s | bias << 8 | f << 20
+        sym[v] = _mm256_and_si256(e, vff);
+        y = _mm256_add_epi32(_mm256_mullo_epi32(_mm256_srli_epi32(e, 20), _mm256_srl_epi32(x[v], vn)),
+                             _mm256_and_si256(_mm256_srli_epi32(e, 8), v12));
+      } else {  // f | bias << 16, symbol separately
+        sym[v] = _mm256_i32gather_epi32(reinterpret_cast<const int *>(tb.symw.data()), slot, 4);
+        y = _mm256_add_epi32(_mm256_mullo_epi32(_mm256_and_si256(e, v16), _mm256_srl_epi32(x[v], vn)),
+                             _mm256_srli_epi32(e, 16));
+      }
+      x[v] = _mm256_blendv_epi8(x[v], y, in[v]);
+    }
+    const uint64_t i0s = (uint64_t)g * kLanes;
+    if (i0s + 31 < t.commit_lo || i0s > t.commit_hi) continue;
+    // 32 symbols (u32) -> 32 bytes in lane order
+    const __m256i p = _mm256_packus_epi16(_mm256_packus_epi32(sym[0], sym[1]), _mm256_packus_epi32(sym[2], sym[3]));
+    const __m256i bytes = _mm256_permutevar8x32_epi32(p, order);
+    uint8_t *dst = out + (i0s - out_base);
+    if (i0s >= t.commit_lo && i0s + 31 <= t.commit_hi) {
+      _mm256_storeu_si256(reinterpret_cast<__m256i *>(dst), bytes);
+    } else {
+      alignas(32) uint8_t b[32];
+      _mm256_store_si256(reinterpret_cast<__m256i *>(b), bytes);
+      for (uint32_t j = 0; j < kLanes; ++j)
+        if (i0s + j >= t.commit_lo && i0s + j <= t.commit_hi) dst[j] = b[j];
+    }
+  }
+  if (t.end_cursor != kNoEndCheck) {
+    if (!avx2_refill(x, cur, w, pm)) return RECOIL_E_UNDERFLOW;  // outputs emitted before group 0 (n = 16, f = 1)
+    if (cur != t.end_cursor) return RECOIL_E_SYNC;
+    for (int v = 0; v < 4; ++v) {
+      const __m256i bad = _mm256_andnot_si256(_mm256_cmpeq_epi32(x[v], vL), in[v]);
+      if (!_mm256_testz_si256(bad, bad)) return RECOIL_E_SYNC;
+    }
+  }
+  return RECOIL_OK;
+}
+
+bool have_avx2() {
+  static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("popcnt");
+  return ok;
+}
+
 bool have_avx512() {
   static const bool ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
                          __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512vbmi2");
@@ -192,7 +307,11 @@ extern "C" int recoil_decode_cpu_ex(const uint8_t *container, uint64_t len, uint
     }
     Tables tb;
     const uint32_t n = d.c->n;
-    const bool simd = !(flags & RECOIL_CPU_SCALAR) && have_avx512();
+    // ISA: AVX-512 when the CPU has it, else AVX2; RECOIL_CPU_AVX2 forces AVX2, RECOIL_CPU_SCALAR scalar
+    const int isa = (flags & RECOIL_CPU_SCALAR) ? 0 : (!(flags & RECOIL_CPU_AVX2) && have_avx512()) ? 2
+                                                                                                   : have_avx2() ? 1 : 0;
+    if ((flags & RECOIL_CPU_AVX2) && !(flags & RECOIL_CPU_SCALAR) && !have_avx2()) return RECOIL_E_UNSUPPORTED;
+    const bool simd = isa != 0;
     tb.sym.resize(1u << n);
     tb.f.resize(1u << n);
     tb.bias.resize(1u << n);
@@ -218,7 +337,7 @@ extern "C" int recoil_decode_cpu_ex(const uint8_t *container, uint64_t len, uint
       F += d.c->f[s];
     }
     // the container's words as a host u16 array (little-endian host)
-    std::vector<uint16_t> w(d.c->B + 1);
+    std::vector<uint16_t> w(d.c->B + 16);  // + padding: the AVX2 refill loads 8 words at a time
     if (d.c->B) std::memcpy(w.data(), d.c->words, 2 * d.c->B);
     const uint16_t *slice = w.data() + d.plan.word_lo;
     if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
@@ -227,7 +346,9 @@ extern "C" int recoil_decode_cpu_ex(const uint8_t *container, uint64_t len, uint
     std::atomic<int> err{RECOIL_OK};
     auto worker = [&]() {
       for (size_t k; (k = next.fetch_add(1)) < d.tasks.size() && err.load() == RECOIL_OK;) {
-        int r = simd ? decode_task_avx512(d, tb, d.tasks[k], slice, out) : decode_task(d, tb, d.tasks[k], slice, out);
+        int r = isa == 2   ? decode_task_avx512(d, tb, d.tasks[k], slice, out)
+                : isa == 1 ? decode_task_avx2(d, tb, d.tasks[k], slice, out)
+                           : decode_task(d, tb, d.tasks[k], slice, out);
         if (r) err.store(r);
       }
     };
@@ -245,4 +366,4 @@ extern "C" int recoil_decode_cpu(const uint8_t *container, uint64_t len, uint8_t
   return recoil_decode_cpu_ex(container, len, out, threads, 0);
 }
 
-extern "C" int recoil_cpu_simd(void) { return have_avx512() ? 1 : 0; }
+extern "C" int recoil_cpu_simd(void) { return have_avx512() ? 2 : have_avx2() ? 1 : 0; }

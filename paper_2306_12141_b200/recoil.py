@@ -209,6 +209,7 @@ def recoil_decode_cpu(container, threads: int = 0, out: np.ndarray | None = None
 
 
 RECOIL_CPU_SCALAR = 1
+RECOIL_CPU_AVX2 = 2
 
 
 def recoil_decode_cpu_ex(container, threads: int = 0, flags: int = 0, out: np.ndarray | None = None) -> np.ndarray:
@@ -220,8 +221,13 @@ def recoil_decode_cpu_ex(container, threads: int = 0, flags: int = 0, out: np.nd
     return out
 
 
-def recoil_cpu_simd() -> bool:
-    return bool(load().recoil_cpu_simd())
+def recoil_cpu_simd() -> int:
+    """2 = AVX-512, 1 = AVX2, 0 = scalar (the task decoder recoil_decode_cpu uses here)."""
+    return int(load().recoil_cpu_simd())
+
+
+def recoil_cpu_isa() -> str:
+    return {2: "avx512", 1: "avx2", 0: "scalar"}[recoil_cpu_simd()]
 
 
 def recoil_decode_occupancy(device: int, prob_bits: int) -> tuple[int, int]:

@@ -207,11 +207,12 @@ def test_decoder_plan_layout():
     R.recoil_decoder_destroy(h)
 
 
-@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX-512 F/BW/VL/VBMI2")
+@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX2 and AVX-512")
 @pytest.mark.parametrize("n", list(range(1, 17)))
 def test_avx512_cpu_decoder_matches_scalar_and_input(n):
-    """NEXT row 3: the AVX-512 task decoder (expand-load refill + LUT gathers) equals the
-    scalar decoder and the input, for every n (packed LUT n <= 12, split tables above)."""
+    """NEXT row 3: the SIMD task decoders -- AVX-512 (expand-load refill + LUT gathers) and
+    AVX2 (8 lanes x 4: per-vector word run + mask-indexed permutation) -- equal the scalar
+    decoder and the input, for every n (packed LUT n <= 12, split tables above)."""
     kind = ("exp", "text", "image")[n % 3]
     sym = synth.workload(kind, 400_001 + 37 * n, seed=100 + n, lam=50)
     hist = synth.histogram(sym)
@@ -223,12 +224,14 @@ def test_avx512_cpu_decoder_matches_scalar_and_input(n):
         c = R.recoil_encode(sym, f, n, M)
         a = R.recoil_decode_cpu_ex(c, 4, 0)
         b = R.recoil_decode_cpu_ex(c, 4, R.RECOIL_CPU_SCALAR)
-        assert (a == sym).all() and (b == sym).all()
+        v = R.recoil_decode_cpu_ex(c, 4, R.RECOIL_CPU_AVX2)
+        assert (a == sym).all() and (b == sym).all() and (v == sym).all()
     p = R.recoil_partitioned_encode(sym, f, n, 13)
     assert (R.recoil_decode_cpu_ex(p, 3, 0) == sym).all()
+    assert (R.recoil_decode_cpu_ex(p, 3, R.RECOIL_CPU_AVX2) == sym).all()
 
 
-@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX-512 F/BW/VL/VBMI2")
+@pytest.mark.skipif(not R.recoil_cpu_simd(), reason="CPU lacks AVX2 and AVX-512")
 def test_avx512_cpu_decoder_edges_and_corruption():
     rng = np.random.default_rng(8)
     hist = np.zeros(256, dtype=np.uint64)
@@ -240,10 +243,12 @@ def test_avx512_cpu_decoder_edges_and_corruption():
     sym[:32] = rare[0]  # n = 16 emissions before group 0
     for c in (R.recoil_encode(sym, f, 16, 5), R.recoil_partitioned_encode(sym, f, 16, 7)):
         assert (R.recoil_decode_cpu_ex(c, 2, 0) == sym).all()
+        assert (R.recoil_decode_cpu_ex(c, 2, R.RECOIL_CPU_AVX2) == sym).all()
     for N in (0, 1, 31, 32, 33, 95):  # empty / ragged groups
         s = synth.text_bytes(N, N)
         ff = oracle.build_model(synth.histogram(s) if N else np.ones(256, dtype=np.uint64), 11)
-        assert (R.recoil_decode_cpu_ex(R.recoil_encode(s, ff, 11, 3), 1, 0) == s).all()
+        for flags in (0, R.RECOIL_CPU_AVX2):
+            assert (R.recoil_decode_cpu_ex(R.recoil_encode(s, ff, 11, 3), 1, flags) == s).all()
     s = synth.text_bytes(300000, 9)
     ff = oracle.build_model(synth.histogram(s), 11)
     c = R.recoil_encode(s, ff, 11, 16)
@@ -252,13 +257,13 @@ def test_avx512_cpu_decoder_edges_and_corruption():
     hdr = len(c) - 2 * info["n_words"]
     bad[hdr + 2 * (info["n_words"] // 2)] ^= 0x5A  # flip a bitstream word
     errs = []
-    for flags in (0, R.RECOIL_CPU_SCALAR):
+    for flags in (0, R.RECOIL_CPU_SCALAR, R.RECOIL_CPU_AVX2):
         try:
             out = R.recoil_decode_cpu_ex(bad, 2, flags)
             errs.append(("ok", int((out != s).sum() > 0)))
         except R.RecoilError as e:
             errs.append(("err", e.rc))
-    assert errs[0] == errs[1]  # same verdict from both decoders
+    assert errs[0] == errs[1] == errs[2]  # same verdict from every decoder
 
 
 def _ad_random_models(rng, n, K, max_len=300):
