@@ -398,7 +398,7 @@ def main():
     # ---------------- setup (untimed): rank 0 synthesises and encodes once ----------------
     t_setup = time.perf_counter()
     sym = f_model = None
-    share = None
+    share = os.path.join(tempfile.gettempdir(), f"recoil_bench_{os.environ.get('MASTER_PORT', '0')}.bin")
     enc_s = 0.0
     if rank == 0:
         sym = make_stream(cfg, N_total, args.lam)
@@ -412,7 +412,6 @@ def main():
             c_enc = R.recoil_encode(sym, f, 11, per_gpu_splits * world)
         enc_s = time.perf_counter() - t0
         if world > 1:
-            share = os.path.join(tempfile.gettempdir(), f"recoil_bench_{os.environ.get('MASTER_PORT', '0')}.bin")
             c_enc.tofile(share)
     if world > 1:
         pg.barrier()
