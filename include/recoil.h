@@ -299,6 +299,66 @@ int recoil_pipeline_launches(const recoil_pipeline *p);
 void recoil_pipeline_destroy(recoil_pipeline *p);
 
 /* ---------------------------------------------------------------------- */
+/* On-device metadata path          */
+/* ---------------------------------------------------------------------- */
+
+/* The client copies the received container to the GPU unchanged; the split
+ * metadata is decoded there (global series, split-record offsets, LUT, task
+ * heads) and the decode kernel reads the records in place.  The host reads
+ * only the fixed header and the model block.  Whole stream, "RCL1" only. */
+typedef struct recoil_device_decoder recoil_device_decoder;
+typedef struct {
+  uint64_t container_offset; /* copy the container to d_buffer + container_offset (puts its words 512-B aligned) */
+  uint64_t buffer_bytes;     /* d_buffer size: offset + container + zeroed word padding (>= 256 words + 256 B) */
+  uint64_t workspace_bytes;  /* d_workspace size (status, parse results, LUT, task heads) */
+  uint64_t out_count;        /* d_out bytes (N rounded up to 16) */
+  uint64_t n_symbols;        /* N */
+  uint32_t n_tasks;          /* split tasks (M; 0 for N = 0) */
+  uint32_t prob_bits;        /* n */
+} recoil_device_plan;
+
+/* head: the first head_len bytes of the container (the 28-byte header and the
+ * model block at least: 30 + 5 x symbols); container_len: its full length.
+ * Errors: E_ARG, E_BAD_MAGIC, E_VERSION, E_TRUNCATED, E_INCONSISTENT (header or
+ * model), E_UNSUPPORTED ("RCA1" / "RCV1", more than ~23 MB of split metadata,
+ * a word stream of >= 2^31 words), E_NOMEM. */
+int recoil_device_decoder_create(const uint8_t *head, uint64_t head_len, uint64_t container_len,
+                                 recoil_device_decoder **out);
+int recoil_device_decoder_plan(const recoil_device_decoder *dec, recoil_device_plan *plan);
+/* Convenience H2D (stream-ordered): container -> d_buffer + container_offset, and the
+ * zero padding after it.  A caller that copies the container itself must zero
+ * buffer_bytes - container_offset - container_len bytes after it. */
+int recoil_device_upload(const recoil_device_decoder *dec, const uint8_t *container, void *d_buffer, void *cuda_stream);
+/* Stream-ordered: the metadata kernels, then the decode kernel, writing the N
+ * symbols to d_out[0, N) (it may write d_out up to out_count).  Metadata that
+ * fails its checks (offsets out of range or not increasing, record list not
+ * ending at the words, widths out of range) sets E_INCONSISTENT in the status
+ * word and no task decodes.  Errors: E_ARG, E_CUDA. */
+int recoil_device_decode(recoil_device_decoder *dec, void *d_buffer, void *d_workspace, uint8_t *d_out,
+                         void *cuda_stream);
+/* As recoil_decoder_status for the last recoil_device_decode. */
+int recoil_device_decoder_status(recoil_device_decoder *dec, const void *d_workspace, void *cuda_stream,
+                                 uint64_t *bad_task);
+/* Kernel launches one recoil_device_decode issues. */
+int recoil_device_decoder_launches(const recoil_device_decoder *dec);
+void recoil_device_decoder_destroy(recoil_device_decoder *dec);
+
+/* Combine on the GPU (the server shrinks parallelism per
+ * client): the result of recoil_combine_splits(container, target_splits),
+ * written from the device copy d_in (in_len bytes, any alignment) to d_out.
+ * recoil_device_combine_plan: the d_out capacity and d_workspace size to
+ * provide.  recoil_device_combine writes the output length to the device word
+ * *d_out_len (stream-ordered); it synchronises the stream once (the new
+ * series widths size the output).  target_splits >= M: a copy.  Errors: as
+ * recoil_device_decoder_create, E_BUFFER (capacity), E_INCONSISTENT
+ * (metadata checks), E_OVERFLOW, E_CUDA. */
+int recoil_device_combine_plan(const uint8_t *head, uint64_t head_len, uint64_t container_len, uint32_t target_splits,
+                               uint64_t *out_capacity, uint64_t *workspace_bytes);
+int recoil_device_combine(const uint8_t *head, uint64_t head_len, const uint8_t *d_in, uint64_t in_len,
+                          uint32_t target_splits, uint8_t *d_out, uint64_t out_capacity, void *d_workspace,
+                          uint64_t *d_out_len, void *cuda_stream);
+
+/* ---------------------------------------------------------------------- */
 /* Multi-GPU sharding (host planning; each GPU decodes its own task range) */
 /* ---------------------------------------------------------------------- */
 

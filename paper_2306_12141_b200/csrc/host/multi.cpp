@@ -54,9 +54,11 @@ const NcclApi &nccl() {
 
 int plan_shards(const uint8_t *container, uint64_t len, uint32_t n_dev, std::vector<Decoder> *dec) {
   auto c = std::make_shared<Container>();
-  int rc = parse_container(container, len, c.get(), /*light=*/true);
+  // full parse: the shards use the host-expanded task records, as recoil_decoder_create
+  if (container && len >= 4 && std::memcmp(container, "RCA1", 4) == 0)
+    return RECOIL_E_UNSUPPORTED;  // needs per-device model ids (recoil_decode_adaptive)
+  int rc = parse_container(container, len, c.get(), /*light=*/false);
   if (rc) return rc;
-  if (c->adaptive) return RECOIL_E_UNSUPPORTED;  // needs per-device model ids (recoil_decode_adaptive)
   std::vector<uint64_t> bounds(n_dev + 1, 0);
   shard_bounds_range(*c, 0, c->M, n_dev, bounds.data());
   dec->clear();

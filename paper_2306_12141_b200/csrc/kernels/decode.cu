@@ -987,6 +987,9 @@ extern "C" int recoil_decoder_upload(recoil_decoder *dec, void *d_workspace, uin
 }
 
 namespace recoil {
+int launch_decode(Decoder *d, char *ws, const uint16_t *d_words, uint8_t *d_out, void *stream) {
+  return launch(d, ws, d_words, nullptr, d_out, reinterpret_cast<cudaStream_t>(stream));
+}
 // recoil_decode without the status reset: the caller uploaded a zeroed status
 // block with the workspace on the same stream order (the e2e pipeline's one
 // H2D of tables + records per chunk)

@@ -149,6 +149,8 @@ int build_decoder_from(std::shared_ptr<const Container> c, uint64_t task_begin, 
 // recoil_decode for a workspace whose zeroed status block was uploaded with it
 // (no reset; decode.cu).
 int decode_staged(Decoder *d, char *ws, const uint16_t *d_words, uint8_t *d_out, void *stream);
+// Launch the decode kernel of a prepared plan (no status reset, no single-symbol shortcut).
+int launch_decode(Decoder *d, char *ws, const uint16_t *d_words, uint8_t *d_out, void *stream);
 // Contiguous task ranges with ~equal committed symbols (recoil_shard_plan).
 void shard_bounds(const Container &c, uint32_t n_shards, uint64_t *bounds);
 void shard_bounds_range(const Container &c, uint64_t task_begin, uint64_t task_end, uint32_t n_shards,

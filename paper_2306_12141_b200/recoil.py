@@ -36,7 +36,10 @@ EXPORTS = [
     "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
     "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive", "recoil_decoder_create_subset",
     "recoil_decoder_create_grouped", "recoil_pipeline_run_at", "recoil_pipeline_span", "recoil_multi_plan",
-    "recoil_multi_decode", "recoil_multi_nccl_available",
+    "recoil_multi_decode", "recoil_multi_nccl_available", "recoil_device_decoder_create",
+    "recoil_device_decoder_plan", "recoil_device_upload", "recoil_device_decode", "recoil_device_decoder_status",
+    "recoil_device_decoder_launches", "recoil_device_decoder_destroy", "recoil_device_combine_plan",
+    "recoil_device_combine",
 ]
 
 
@@ -53,6 +56,15 @@ class recoil_info(ctypes.Structure):
                 ("header_bytes", ctypes.c_uint64), ("meta_bytes", ctypes.c_uint64),
                 ("word_bytes", ctypes.c_uint64), ("total_bytes", ctypes.c_uint64),
                 ("symbol_bits", ctypes.c_uint32), ("n_models", ctypes.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class recoil_device_plan(ctypes.Structure):
+    _fields_ = [("container_offset", ctypes.c_uint64), ("buffer_bytes", ctypes.c_uint64),
+                ("workspace_bytes", ctypes.c_uint64), ("out_count", ctypes.c_uint64), ("n_symbols", ctypes.c_uint64),
+                ("n_tasks", ctypes.c_uint32), ("prob_bits", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -115,6 +127,15 @@ def load(path: str = LIB_PATH):
         "recoil_multi_plan": (i32, [P, u64, u32, P]),
         "recoil_multi_decode": (i32, [P, u64, u32, P, P, i32, P, P]),
         "recoil_multi_nccl_available": (i32, []),
+        "recoil_device_decoder_create": (i32, [P, u64, u64, P]),
+        "recoil_device_decoder_plan": (i32, [P, P]),
+        "recoil_device_upload": (i32, [P, P, P, P]),
+        "recoil_device_decode": (i32, [P, P, P, P, P]),
+        "recoil_device_decoder_status": (i32, [P, P, P, P]),
+        "recoil_device_decoder_launches": (i32, [P]),
+        "recoil_device_decoder_destroy": (None, [P]),
+        "recoil_device_combine_plan": (i32, [P, u64, u64, u32, P, P]),
+        "recoil_device_combine": (i32, [P, u64, P, u64, u32, P, u64, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -514,6 +535,84 @@ def decode_gpu(container, device: int = 0):
     out = dec.output().clone()
     dec.close()
     return out
+
+
+# --- on-device metadata path (NEXT 2): the container goes to the GPU as it is -------------
+
+class DeviceContainerDecoder:
+    """recoil_device_*: the host reads the fixed header + model block only; the container is
+    copied to the GPU unchanged and its split metadata decoded there (global series, record
+    offsets, LUT, task heads), then the decode kernel runs.  Device buffers are torch tensors."""
+
+    def __init__(self, container, device: int = 0, stream=None):
+        import torch
+        c = _u8(container)
+        self.container = c
+        self.device = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        _check(load().recoil_device_decoder_create(c.ctypes.data, c.size, c.size, ctypes.byref(h)),
+               "recoil_device_decoder_create")
+        self.handle = h
+        pl = recoil_device_plan()
+        _check(load().recoil_device_decoder_plan(h, ctypes.byref(pl)), "recoil_device_decoder_plan")
+        self.plan = pl.as_dict()
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        self.buffer = torch.empty(self.plan["buffer_bytes"], dtype=torch.uint8, device=self.device)
+        self.workspace = torch.empty(max(self.plan["workspace_bytes"], 256), dtype=torch.uint8, device=self.device)
+        self.out = torch.empty(max(self.plan["out_count"], 16), dtype=torch.uint8, device=self.device)
+
+    def upload(self, container=None) -> None:
+        """H2D of the container bytes (pinned for an asynchronous copy) + zero padding."""
+        c = self.container if container is None else container
+        ptr = c.data_ptr() if hasattr(c, "data_ptr") else _u8(c).ctypes.data
+        _check(load().recoil_device_upload(self.handle, ptr, self.buffer.data_ptr(), self.stream.cuda_stream),
+               "recoil_device_upload")
+
+    def decode(self) -> None:
+        _check(load().recoil_device_decode(self.handle, self.buffer.data_ptr(), self.workspace.data_ptr(),
+                                           self.out.data_ptr(), self.stream.cuda_stream), "recoil_device_decode")
+
+    def status(self):
+        bad = ctypes.c_uint64(0)
+        rc = load().recoil_device_decoder_status(self.handle, self.workspace.data_ptr(), self.stream.cuda_stream,
+                                                 ctypes.byref(bad))
+        return rc, (None if bad.value == (1 << 64) - 1 else bad.value)
+
+    def output(self):
+        return self.out[:self.plan["n_symbols"]]
+
+    def launches(self) -> int:
+        return _check(load().recoil_device_decoder_launches(self.handle), "recoil_device_decoder_launches")
+
+    def close(self) -> None:
+        if self.handle:
+            load().recoil_device_decoder_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def recoil_device_combine(container, d_in, target_splits: int, stream=None):
+    """Combine on the GPU: d_in (torch uint8 tensor holding `container`) -> a new device tensor
+    with the combined container (recoil_combine_splits(container, target_splits) byte for byte)."""
+    import torch
+    c = _u8(container)
+    cap, wsb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(load().recoil_device_combine_plan(c.ctypes.data, c.size, c.size, target_splits, ctypes.byref(cap),
+                                             ctypes.byref(wsb)), "recoil_device_combine_plan")
+    out = torch.empty(cap.value, dtype=torch.uint8, device=d_in.device)
+    ws = torch.empty(max(wsb.value, 256), dtype=torch.uint8, device=d_in.device)
+    n = torch.zeros(1, dtype=torch.int64, device=d_in.device)
+    st = stream or torch.cuda.current_stream(d_in.device)
+    _check(load().recoil_device_combine(c.ctypes.data, c.size, d_in.data_ptr(), c.size, target_splits,
+                                        out.data_ptr(), cap.value, ws.data_ptr(), n.data_ptr(), st.cuda_stream),
+           "recoil_device_combine")
+    st.synchronize()
+    return out[:int(n.item())]
 
 
 # --- multi-GPU (§8(e), row a10): optional gather of the shards' spans ----------------------

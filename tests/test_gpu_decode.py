@@ -490,7 +490,13 @@ def test_crafted_record_cannot_write_outside_the_plan():
     c = R.recoil_encode(sym, f, 11, 512)
     assert bytes(_move_max_group(c, 105, 0)) == bytes(c)  # the re-serialiser is exact
     bad = _move_max_group(c, 105, 2000)  # point 105 = the entry of task 105, inside the plan [100, 110)
-    dec = R.GpuDecoder(bad, 0, 100, 110)
+    # the default plan parses every record on the host (full parse) and rejects the container
+    with pytest.raises(R.RecoilError) as ei:
+        R.GpuDecoder(bad, 0, 100, 110)
+    assert ei.value.rc == R.RECOIL_E_INCONSISTENT
+    # the light-parse plans (decoder-side subset, e2e pipeline chunks) expand the records in the
+    # kernel: there the kernel's window check must catch it
+    dec = R.GpuDecoder(bad, 0, 100, 110, subset=512)
     guard = 1 << 20
     assert 2000 * 32 < guard
     big = torch.full((dec.plan["out_count"] + 2 * guard,), 0xAB, dtype=torch.uint8, device="cuda")
@@ -501,6 +507,16 @@ def test_crafted_record_cannot_write_outside_the_plan():
     assert R.ERRORS.get(rc) == "RECOIL_E_INCONSISTENT"
     host = big.cpu().numpy()
     assert (host[:guard] == 0xAB).all() and (host[-guard:] == 0xAB).all()
+    # the on-device metadata path checks the sync starts on the GPU and skips the tasks
+    dd = R.DeviceContainerDecoder(bad, 0)
+    big = torch.full((dd.plan["out_count"] + 2 * guard,), 0xAB, dtype=torch.uint8, device="cuda")
+    dd.out = big[guard:guard + dd.plan["out_count"]]
+    dd.upload()
+    dd.decode()
+    assert R.ERRORS.get(dd.status()[0]) == "RECOIL_E_INCONSISTENT"
+    host = big.cpu().numpy()
+    assert (host[:guard] == 0xAB).all() and (host[-guard:] == 0xAB).all()
+    dd.close()
 
 
 @pytest.mark.timeout(900)

@@ -1,0 +1,140 @@
+"""On-device metadata path: the container goes to
+the GPU unchanged, the split metadata is decoded there (global series, split-record
+offsets by a speculative chunked parse, LUT, task heads) and the decode kernel reads the
+records in place.  Every output byte is compared with the input (the decode's definition)
+and with the oracle's decode; the GPU combine is compared byte for byte with the oracle's
+combine (O8) and the library's."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2306_12141_b200 import recoil as R
+
+pytestmark = pytest.mark.gpu
+
+
+def _enc(kind, n, M, nbits=11, seed=3):
+    sym = synth.workload(kind, n, seed=seed, lam=50)
+    hist = synth.histogram(sym) if n else np.ones(256, np.uint64)
+    if (hist > 0).sum() > (1 << nbits):
+        sym = (sym % (1 << min(nbits, 8))).astype(np.uint8)
+        hist = synth.histogram(sym)
+    f = R.recoil_build_model(hist, nbits)
+    return sym, R.recoil_encode(sym, f, nbits, M)
+
+
+def _device_decode(c):
+    dd = R.DeviceContainerDecoder(c, 0)
+    dd.upload()
+    dd.decode()
+    rc, bad = dd.status()
+    out = dd.output().cpu().numpy()
+    dd.close()
+    return rc, bad, out
+
+
+@pytest.mark.parametrize("kind,n,M", [("exp", 1 << 20, 16), ("text", 3_000_017, 700), ("image", 5_000_000, 4000),
+                                      ("exp", 100_000, 1), ("text", 33, 3), ("exp", 0, 5), ("image", 2_000_000, 20000)])
+def test_device_parse_decodes_bit_exact(kind, n, M):
+    sym, c = _enc(kind, n, M)
+    rc, bad, out = _device_decode(c)
+    assert rc == 0, (R.ERRORS.get(rc), bad)
+    assert np.array_equal(out, sym)
+    if n and n <= 3_000_017:
+        assert np.array_equal(oracle.recoil_decode(c.tobytes()), out)
+
+
+@pytest.mark.parametrize("nbits", [1, 4, 9, 12, 13, 16])
+def test_device_parse_every_lut_form(nbits):
+    sym, c = _enc("exp", 400_001, 97, nbits, seed=nbits)
+    rc, _, out = _device_decode(c)
+    assert rc == 0 and np.array_equal(out, sym)
+
+
+def test_device_parse_many_chunks_and_wide_records():
+    """65536 splits: ~5 MB of records over hundreds of parse chunks (config 4's encode)."""
+    sym, c = _enc("exp", 1 << 26, 65536)
+    assert R.recoil_inspect(c)["n_splits"] == 65536
+    rc, _, out = _device_decode(c)
+    assert rc == 0 and np.array_equal(out, sym)
+
+
+def test_device_parse_single_symbol_model():
+    sym = np.full(100_000, 7, np.uint8)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 8)
+    rc, _, out = _device_decode(c)
+    assert rc == 0 and np.array_equal(out, sym)
+
+
+def test_device_parse_matches_host_plan_on_corrupt_metadata():
+    """Bytes flipped anywhere in the metadata (global series, anchor states, width fields):
+    the device parse must agree with the host parse -- where the host rejects the container
+    (E_INCONSISTENT / E_TRUNCATED) the device flags E_INCONSISTENT; where the host plans it,
+    the device decode gives the same status and the same bytes.  (The format has no checksum:
+    a flipped anchor state may decode to wrong bytes on both paths.)  Never a fault."""
+    sym, c = _enc("text", 2_000_000, 500)
+    info = R.recoil_inspect(c)
+    meta_lo = info["header_bytes"] + 128
+    meta_hi = len(c) - 2 * info["n_words"]
+    rng = np.random.default_rng(5)
+    flagged = 0
+    for trial in range(40):
+        cc = c.copy()
+        pos = int(rng.integers(meta_lo, meta_hi)) if trial % 4 else int(rng.integers(meta_lo, meta_lo + 400))
+        cc[pos] ^= np.uint8(1 << int(rng.integers(0, 8)))
+        rc, _, out = _device_decode(cc)
+        try:
+            dec = R.GpuDecoder(cc, 0)
+        except R.RecoilError as e:
+            assert e.rc in (R.RECOIL_E_INCONSISTENT, R.RECOIL_E_TRUNCATED), e
+            assert rc == R.RECOIL_E_INCONSISTENT, (pos, rc)
+            flagged += 1
+            continue
+        dec.upload()
+        dec.decode()
+        hrc, _ = dec.status()
+        hout = dec.output().cpu().numpy()
+        dec.close()
+        assert rc == hrc, (pos, rc, hrc)
+        if rc == 0:
+            assert np.array_equal(out, hout), pos
+        else:
+            flagged += 1
+    assert flagged > 0
+
+
+def test_device_parse_rejects_other_containers():
+    sym = synth.workload("exp", 10_000, seed=1, lam=50)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    p = R.recoil_partitioned_encode(sym, f, 11, 4)
+    with pytest.raises(R.RecoilError):
+        R.DeviceContainerDecoder(p, 0)
+    with pytest.raises(R.RecoilError):
+        R.DeviceContainerDecoder(np.zeros(64, np.uint8), 0)
+
+
+@pytest.mark.parametrize("kind,n,M,targets", [("exp", 1 << 22, 2048, [1, 2, 16, 300, 2047, 2048, 5000]),
+                                              ("text", 777_777, 97, [1, 3, 50, 96]),
+                                              ("image", 1 << 24, 20000, [2048, 256, 16])])
+def test_device_combine_equals_oracle_and_library(kind, n, M, targets):
+    sym, c = _enc(kind, n, M)
+    d_in = torch.from_numpy(c).cuda()
+    for t in targets:
+        got = R.recoil_device_combine(c, d_in, t).cpu().numpy()
+        lib = R.recoil_combine_splits(c, t)
+        assert np.array_equal(got, lib), t
+        if n <= (1 << 22):
+            assert got.tobytes() == oracle.combine(c.tobytes(), t), t
+        rc, _, out = _device_decode(got)
+        assert rc == 0 and np.array_equal(out, sym), t
+
+
+def test_device_combine_config4_65536_to_2048_256_16():
+    sym, c = _enc("exp", 1 << 26, 65536)
+    d_in = torch.from_numpy(c).cuda()
+    for t in (2048, 256, 16):
+        got = R.recoil_device_combine(c, d_in, t).cpu().numpy()
+        assert np.array_equal(got, R.recoil_combine_splits(c, t)), t
