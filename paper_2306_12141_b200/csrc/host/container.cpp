@@ -278,7 +278,8 @@ int parse_container(const uint8_t *c, uint64_t len, Container *o, bool light) {
   o->sync_start.resize(P);
   o->bidx.resize(P);
   for (uint64_t k = 0; k < P; ++k) {
-    if (o->offset[k] >= o->B || o->maxg[k] >= o->G) return RECOIL_E_INCONSISTENT;
+    if (o->offset[k] >= o->B || o->maxg[k] >= o->G || (k && o->offset[k] <= o->offset[k - 1]))
+      return RECOIL_E_INCONSISTENT;
     // anchor index of lane j = (maxg - d_j) W + j: its min / max over lanes via d_j W - j
     const uint16_t *gd = &o->gdiff[k * W];
     int32_t dmax = 0, vmax = INT32_MIN, vmin = INT32_MAX;

@@ -2,7 +2,7 @@
 committed summaries under profiles/ and the per-launch numbers bench.py reads
 (profiles/ncu_traffic.json): DRAM bytes and shared-memory wavefronts per launch.
 
-usage: python tools/refresh_profiles.py TAG config2:7104 config1:16 config3:14208 ...
+usage: python tools/refresh_profiles.py [--round=r02] TAG config5:10656 config3:10656 ...
 """
 import csv
 import io
@@ -24,7 +24,37 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-        "sm__inst_executed.sum", "launch__shared_mem_per_block_static"]
+        "sm__inst_executed.sum", "launch__shared_mem_per_block_static",
+        "smsp__average_warp_latency_issue_stalled_short_scoreboard.ratio",
+        "smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio",
+        "smsp__average_warp_latency_issue_stalled_wait.ratio",
+        "smsp__average_warp_latency_issue_stalled_not_selected.ratio",
+        "smsp__average_warp_latency_issue_stalled_mio_throttle.ratio",
+        "smsp__average_warp_latency_issue_stalled_math_pipe_throttle.ratio",
+        "smsp__average_warp_latency_issue_stalled_lg_throttle.ratio",
+        "smsp__average_warp_latency_issue_stalled_selected.ratio",
+        "smsp__average_warp_latency_issue_stalled_barrier.ratio",
+        "smsp__average_warp_latency_issue_stalled_membar.ratio",
+        "smsp__average_warp_latency_issue_stalled_branch_resolving.ratio",
+        "smsp__average_warp_latency_issue_stalled_dispatch_stall.ratio",
+        "smsp__average_warp_latency_issue_stalled_no_instruction.ratio",
+        "smsp__average_warp_latency_issue_stalled_drain.ratio",
+        "smsp__average_warp_latency_issue_stalled_sleeping.ratio",
+        "smsp__warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+        "smsp__warps_issue_stalled_selected_per_issue_active.ratio",
+        "smsp__inst_executed_op_shared_ld.sum", "smsp__inst_executed_op_shared_st.sum",
+        "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__mio_inst_issued.avg.pct_of_peak_sustained_active", "sm__mio_pq_read_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__mio2rf_writeback_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_issued.avg.per_cycle_active", "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_adu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_cbu.avg.pct_of_peak_sustained_active"]
 
 
 def summary(rep):
@@ -45,6 +75,9 @@ def summary(rep):
 
 
 def main():
+    rnd = "r02"
+    if sys.argv[1].startswith("--round="):
+        rnd = sys.argv.pop(1).split("=", 1)[1]
     tag = sys.argv[1]
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
@@ -56,7 +89,7 @@ def main():
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{name}_{tag}.ncu-rep")
         s = summary(rep)
         s["source"] = f"ncu --set full --clock-control none, 1 decode launch of bench.py --config {cfg} ({M} splits)"
-        dst = os.path.join(ROOT, "profiles", f"r01_decode_{name}_ncu_full.json")
+        dst = os.path.join(ROOT, "profiles", f"{rnd}_decode_{name}_ncu_full.json")
         json.dump(s, open(dst, "w"), indent=1)
         rd = s["dram__bytes_read.sum"]["value"] * UNIT[s["dram__bytes_read.sum"]["unit"]]
         wr = s["dram__bytes_write.sum"]["value"] * UNIT[s["dram__bytes_write.sum"]["unit"]]
