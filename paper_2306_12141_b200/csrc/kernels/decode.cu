@@ -360,6 +360,14 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const
                                              int init_group, uint32_t state) {
   const int gb = g & ~15, k1 = g_end & 15;
   w.window_check();
+  if constexpr (NB <= 0) {  // adaptive: a loop, not 16 unrolled entries (instruction-cache size, see run_block)
+#pragma unroll 1
+    for (int k = g & 15;; --k) {
+      x = step<NB, SYNC>(w, lut, sym, x, gb + k, k, init_group, state);
+      if (k == k1) break;
+    }
+    return x;
+  }
 #define RECOIL_STEP(K)                                                  \
   x = step<NB, SYNC>(w, lut, sym, x, gb + K, K, init_group, state);     \
   if (k1 == K) break;
@@ -385,14 +393,28 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const
   return x;
 }
 
+#ifndef RECOIL_AD_UNROLL
+#define RECOIL_AD_UNROLL 16
+#endif
+constexpr int kAdUnroll = RECOIL_AD_UNROLL;
 // A whole 16-group block with every lane initialised: no branch per group.
 template <int NB>
 __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x) {
   w.window_check();
+  if constexpr (NB <= 0) {
+    // adaptive: ~60 instructions per group, so a fully unrolled block (and its copies in
+    // the partial-block paths) overflows the instruction cache; unroll by RECOIL_AD_UNROLL
+#pragma unroll kAdUnroll
+    for (int k = 15; k >= 0; --k) {
+      x = w.refill(x);
+      x = w.decode<NB>(lut, sym, x, k);
+    }
+  } else {
 #pragma unroll
-  for (int k = 15; k >= 0; --k) {
-    x = w.refill(x);
-    x = w.decode<NB>(lut, sym, x, k);
+    for (int k = 15; k >= 0; --k) {
+      x = w.refill(x);
+      x = w.decode<NB>(lut, sym, x, k);
+    }
   }
   return x;
 }
