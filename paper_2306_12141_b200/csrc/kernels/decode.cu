@@ -394,7 +394,7 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const
 }
 
 #ifndef RECOIL_AD_UNROLL
-#define RECOIL_AD_UNROLL 16
+#define RECOIL_AD_UNROLL 4
 #endif
 constexpr int kAdUnroll = RECOIL_AD_UNROLL;
 // A whole 16-group block with every lane initialised: no branch per group.
