@@ -351,7 +351,7 @@ def main():
                     help=f"splits per GPU = waves x resident warps; 0 = {WAVES} (DESIGN.md §13)")
     ap.add_argument("--splits", type=int, default=0, help="override the split count per GPU")
     ap.add_argument("--combine-to", type=int, default=2048, help="config4: target split count")
-    ap.add_argument("--chunks", type=int, default=8, help="e2e pipeline chunks per GPU")
+    ap.add_argument("--chunks", type=int, default=16, help="e2e pipeline chunks per GPU")
     ap.add_argument("--streams", type=int, default=3, help="e2e pipeline streams per GPU")
     ap.add_argument("--lam", type=float, default=0.0, help="config3/4: override lambda")
     ap.add_argument("--reps", type=int, default=3, help="alternating Recoil / partitioned repetitions (N = 1)")
