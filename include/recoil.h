@@ -348,8 +348,9 @@ void recoil_device_decoder_destroy(recoil_device_decoder *dec);
  * written from the device copy d_in (in_len bytes, any alignment) to d_out.
  * recoil_device_combine_plan: the d_out capacity and d_workspace size to
  * provide.  recoil_device_combine writes the output length to the device word
- * *d_out_len (stream-ordered); it synchronises the stream once (the new
- * series widths size the output).  target_splits >= M: a copy.  Errors: as
+ * *d_out_len (stream-ordered); it synchronises the stream twice (8-byte
+ * read-backs: the new series widths, then the kept records' total size,
+ * place the series and the word stream).  target_splits >= M: a copy.  Errors: as
  * recoil_device_decoder_create, E_BUFFER (capacity), E_INCONSISTENT
  * (metadata checks), E_OVERFLOW, E_CUDA. */
 int recoil_device_combine_plan(const uint8_t *head, uint64_t head_len, uint64_t container_len, uint32_t target_splits,

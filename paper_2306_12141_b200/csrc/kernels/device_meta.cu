@@ -20,7 +20,7 @@
 // then the decode kernel runs.  recoil_device_combine (the server
 // shrinks parallelism per client) does the same parse and writes the combined
 // container on the GPU: new global series, the kept records copied verbatim
-// (a record depends only on its own point), the word stream.
+// (a record depends only on its own point), the word stream (device-to-device copy).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -433,28 +433,6 @@ __global__ void k_cmb_records(uint64_t P2, uint64_t kstep, const uint8_t *in, co
   for (uint64_t k = lane; k < n; k += 32) out[d + k] = in[a + k];
 }
 
-// the word stream (and any byte range) from in + src to out + dst (device-computed dst offset)
-__global__ void k_cmb_copy(const uint8_t *in, uint64_t src, uint8_t *out, const uint64_t *rec_out, uint64_t P2,
-                           uint64_t dst_base, uint64_t n) {
-  const uint64_t dst = dst_base + rec_out[P2];
-  // 16 output bytes per thread: aligned 16-B stores where the destination allows it
-  const uint64_t head = (16 - ((reinterpret_cast<uintptr_t>(out) + dst) & 15)) & 15;
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  if (tid < min(head, n)) out[dst + tid] = in[src + tid];
-  if (n <= head) return;
-  const uint64_t body = (n - head) / 16;
-  for (uint64_t q = tid; q < body; q += stride) {
-    const uint64_t o = head + 16 * q;
-    alignas(16) uint8_t buf[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) buf[k] = in[src + o + k];
-    *reinterpret_cast<uint4 *>(out + dst + o) = *reinterpret_cast<const uint4 *>(buf);
-  }
-  const uint64_t tail = head + 16 * body;
-  if (tid < n - tail) out[dst + tail + tid] = in[src + tail + tid];
-}
-
 __global__ void k_cmb_total(uint64_t fixed, const uint64_t *rec_out, uint64_t P2, uint64_t words_bytes,
                             unsigned long long *total) {
   *total = fixed + rec_out[P2] + words_bytes;
@@ -791,8 +769,17 @@ extern "C" int recoil_device_combine(const uint8_t *head, uint64_t head_len, con
   dm::k_cmb_scan<<<1, 1024, 0, s>>>(P2, kstep, rec_off, rec_out);
   const uint32_t rb = (uint32_t)std::max<uint64_t>(1, ceil_div(32 * P2, 256));
   dm::k_cmb_records<<<rb, 256, 0, s>>>(P2, kstep, d_in, rec_off, rec_out, rec_base, d_out);
-  dm::k_cmb_copy<<<1184, 256, 0, s>>>(d_in, h.wstart, d_out, rec_out, P2, rec_base, 2 * h.B);
   dm::k_cmb_total<<<1, 1, 0, s>>>(rec_base, rec_out, P2, 2 * h.B, tot);
   if (cudaGetLastError() != cudaSuccess) return RECOIL_E_CUDA;
+  // the word stream follows the kept records: one more 8-byte read-back places it, then a
+  // device-to-device copy (the driver's copy engine handles the byte misalignment)
+  uint64_t rec_bytes = 0;
+  if (cudaMemcpyAsync(&rec_bytes, rec_out + P2, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  if (rec_base + rec_bytes + 2 * h.B > out_capacity) return RECOIL_E_BUFFER;
+  if (h.B && cudaMemcpyAsync(d_out + rec_base + rec_bytes, d_in + h.wstart, 2 * h.B, cudaMemcpyDeviceToDevice, s) !=
+                 cudaSuccess)
+    return RECOIL_E_CUDA;
   return RECOIL_OK;
 }
