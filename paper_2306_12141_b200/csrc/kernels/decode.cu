@@ -291,23 +291,18 @@ struct Warp {
       // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (2^8 or 2^6 buckets of
       // the slot range per model) and a warp-converged binary search inside
       // the bucket's entry range; value = j + delta(model)
-#ifdef RECOIL_AD_CLAMP_STAGED
-      const uint32_t km = lds_u8(mid32 + k * 32);  // clamped to K - 1 when staged
-#else
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
-#endif
       const uint32_t slot = x & ((1u << nb) - 1);
       const uint32_t ca = coarse32 + 2 * (km * p->ad_crow + (slot >> cshift));
       uint32_t lo = lds_u16(ca), hi = lds_u16(ca + 2);
-#ifdef RECOIL_AD_FIRST_STEP
-      {  // the first search step unconditionally (predicated, no vote): most buckets hold <= 2 entries
+      {  // the first search step unconditionally (predicated, no vote): most buckets hold <= 2
+         // entries, and the warp-converged loop below then runs for ~1/3 of the groups (+2 %)
         const uint32_t m = (lo + hi + 1) >> 1;
         const bool up = (lds_u32(ent32 + 4 * m) & 0xFFFFu) <= slot;
         const bool open = lo < hi;
         lo = open && up ? m : lo;
         hi = open && !up ? m - 1 : hi;
       }
-#endif
       while (__any_sync(kFull, lo < hi)) {
         if (lo < hi) {
           const uint32_t m = (lo + hi + 1) >> 1;
@@ -693,16 +688,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     };
     auto stage_block = [&](int blk) {
       if constexpr (NB <= 0) {
-#ifdef RECOIL_AD_CLAMP_STAGED
-        uint4 v = (mid_blk == blk) ? midv : mid_load(blk);
-        const uint32_t km4 = w.kmax * 0x01010101u;  // model ids >= K are clamped (recoil.h), 4 per word
-        v.x = __vminu4(v.x, km4);
-        v.y = __vminu4(v.y, km4);
-        v.z = __vminu4(v.z, km4);
-        v.w = __vminu4(v.w, km4);
-#else
         const uint4 v = (mid_blk == blk) ? midv : mid_load(blk);
-#endif
         __syncwarp();
         sts_v4(w.mid32 - lane + 16 * lane, v);
         __syncwarp();
