@@ -182,6 +182,27 @@ def make_stream(cfg: str, n_total: int, lam_override: float = 0.0, start: int = 
                           start=start)
 
 
+def issue_roofline(prof: dict, avg_ms: float, clocks, sms: int, groups: int):
+    """The other binding resource: warp-instruction issue (plain integer ALU path, no tensor cores).
+    Peak = 4 schedulers x 1 warp-instruction per cycle per SM x SMs x the SM clock sampled during the run
+    (B200_PROFILING.md unit counts).  'achieved' counts the algorithmic instructions: the steady-state
+    20 warp-instructions per 32-symbol group (SASS of the unrolled block) x the launch's
+    groups; 'measured' is ncu's smsp__inst_executed of the same launch (all overheads included)."""
+    if avg_ms <= 0:
+        return None
+    mhz = (clocks.report() or {}).get("sm_mhz") or 1965.0
+    peak = 4 * sms * mhz * 1e6
+    alg = 20 * groups / (avg_ms / 1e3)
+    out = {"bound": "alu", "achieved": round(alg / 1e9, 1), "peak": round(peak / 1e9, 1),
+           "unit": "G warp-instructions/s", "frac": round(alg / peak, 4), "instructions_per_group": 20}
+    inst = prof.get("warp_instructions_per_launch")
+    if inst:
+        out["measured"] = round(inst / (avg_ms / 1e3) / 1e9, 1)
+        out["measured_frac"] = round(inst / (avg_ms / 1e3) / peak, 4)
+        out["measured_instructions_per_group"] = round(inst / max(1, groups), 2)
+    return out
+
+
 def peak_hbm() -> float:
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") or 6650.0)
@@ -728,6 +749,7 @@ def main():
                          "note": "achieved = (decoded bytes written + compressed words read + task table) / "
                                  "event-timed decode (rank 0); peak = MEASURED_PEAKS.json hbm_gbs (burst)"},
             "roofline_smem": smem_roofline(prof, my_avg_ms, clocks, sms),
+            "roofline_issue": issue_roofline(prof, my_avg_ms, clocks, sms, (n_rank + 31) // 32),
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": int(plan["upload_bytes"]), "d2h_bytes_per_step": int(n_rank),

@@ -94,8 +94,10 @@ def main():
         rd = s["dram__bytes_read.sum"]["value"] * UNIT[s["dram__bytes_read.sum"]["unit"]]
         wr = s["dram__bytes_write.sum"]["value"] * UNIT[s["dram__bytes_write.sum"]["unit"]]
         wf = s["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]["value"]
+        inst = s.get("smsp__inst_executed.sum", {}).get("value")
         traffic[f"{cfg}:{M}"] = {"dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
                                  "smem_wavefronts_per_launch": int(wf),
+                                 "warp_instructions_per_launch": int(inst) if inst else None,
                                  "source": os.path.relpath(dst, ROOT) + " (ncu --set full, 1 launch inside bench.py)"}
         print(cfg, M, int(rd + wr), int(wf), s["gpu__time_duration.sum"])
     json.dump(traffic, open(tf, "w"), indent=1)
