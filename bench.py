@@ -583,8 +583,8 @@ def main():
             "device_parse_and_decode_GBs": round(N_total / float(np.mean(dev_ms)) / 1e6, 1),
             "kernel_launches_per_step": int(dd.launches()),
             "note": "recoil_device_upload + recoil_device_decode + D2H: the host reads only the fixed header; "
-                    "global series, split-record offsets (speculative chunked parse), LUT and task heads are "
-                    "decoded on the GPU, records read in place; one stream, wall clock"}
+                    "global series, split-record offsets (speculative chunked parse), LUT and task records are "
+                    "built on the GPU; one stream, wall clock"}
         dd.close()
         del pin_c, host_syms
     if pg and args.gather:
