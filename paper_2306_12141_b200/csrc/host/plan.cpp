@@ -115,8 +115,8 @@ static int build_fused(Decoder *d, uint64_t tb, uint64_t te) {
   const Container &c = *d->c;
   d->fused = true;
   if (c.adaptive) {
-    // 8-bit buckets on the 32-warp kernel when its layout and those tables fit one
-    // block's shared memory, else 6-bit buckets on the 8-warp kernel
+    // the most coarse bucket bits in 9..7 whose tables fit beside the 32-warp kernel's
+    // layout in one block's shared memory, else 6-bit buckets on the 8-warp kernel
     int rc0 = RECOIL_OK;
     d->ad_narrow = true;
     for (uint32_t cb = kCoarseBitsWide; cb >= kCoarseBitsWideMin && d->ad_narrow && !rc0; --cb) {

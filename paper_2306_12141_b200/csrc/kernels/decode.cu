@@ -1098,7 +1098,7 @@ extern "C" int recoil_decode_occupancy_adaptive(int device, uint32_t n_models, u
   if (cudaGetDevice(&prev) != cudaSuccess) return RECOIL_E_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return RECOIL_E_CUDA;
   int per_sm = 0, sms = 0, rc;
-  // the plan's choice (build_fused): 32-warp CTAs with 8-bit buckets if they fit
+  // the plan's choice (build_fused): 32-warp CTAs with 2^9..2^7 buckets if they fit
   uint64_t wide = 0;
   bool narrow = true;
   for (uint32_t cb = kCoarseBitsWide; cb >= kCoarseBitsWideMin && narrow; --cb) {
