@@ -288,7 +288,7 @@ struct Warp {
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
     if constexpr (NB <= 0) {
       // Eq. 2 under model mid(i) (P:227 item (3)): the entry j of the model
-      // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (2^8 or 2^6 buckets of
+      // with F_j <= slot < F_j + f_j, by a coarse bucket lookup (2^9..2^6 buckets of
       // the slot range per model) and a warp-converged binary search inside
       // the bucket's entry range; value = j + delta(model)
       const uint32_t km = min(lds_u8(mid32 + k * 32), kmax);
