@@ -125,10 +125,23 @@ __global__ void k_global(GArgs a, uint64_t *offset, uint32_t *maxg, uint32_t *fi
   maxg[tid] = bad ? 0 : (uint32_t)mg;
 }
 
+// Stage bytes [src, src + n) into shared memory with aligned 16-B loads of the covering range;
+// returns the shared pointer of src's first byte (smbuf must hold n + 32 bytes).  The covering
+// range stays inside the device buffer: the metadata precedes the (padded) word stream.
+__device__ __forceinline__ const uint8_t *stage_bytes(uint8_t *smbuf, const uint8_t *src, uint32_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+  const uint32_t lead = (uint32_t)(reinterpret_cast<uintptr_t>(src) - a);
+  const uint32_t n16 = (lead + n + 15) / 16;
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(smbuf)[i] = reinterpret_cast<const uint4 *>(a)[i];
+  __syncthreads();
+  return smbuf + lead;
+}
+
 // 2a. speculative parse: block t stages chunk t (+ 130 bytes) of the points section and thread e
 // parses from chunk position e; spec[t][e] = end position (chunk relative) | record count << 16
 __global__ void k_spec(const uint8_t *c, uint64_t wstart, uint32_t C, uint32_t T, const Misc *misc, uint32_t *spec) {
-  extern __shared__ uint8_t sm[];
+  extern __shared__ __align__(16) uint8_t smbuf[];
   const uint64_t rpos = misc->rpos;
   const uint64_t Ls = wstart > rpos ? wstart - rpos : 0;
   const uint64_t cs = (uint64_t)blockIdx.x * C;
@@ -137,8 +150,7 @@ __global__ void k_spec(const uint8_t *c, uint64_t wstart, uint32_t C, uint32_t T
     return;
   }
   const uint32_t have = (uint32_t)(Ls - cs < (uint64_t)C + kEntries + 64 ? Ls - cs : (uint64_t)C + kEntries + 64);
-  for (uint32_t i = threadIdx.x; i < have; i += blockDim.x) sm[i] = c[rpos + cs + i];
-  __syncthreads();
+  const uint8_t *sm = stage_bytes(smbuf, c + rpos + cs, have);
   for (uint32_t e = threadIdx.x; e < kEntries; e += blockDim.x) {
     uint32_t p = e, cnt = 0;
     bool bad = false;
@@ -189,15 +201,14 @@ __global__ void k_resolve(uint32_t C, uint32_t T, uint64_t P, uint64_t wstart, c
 // 2c. every chunk writes the offsets of the records that start in it
 __global__ void k_write(const uint8_t *c, uint64_t wstart, uint32_t C, uint64_t P, const uint32_t *chunk,
                         const Misc *misc, uint64_t *rec_off) {
-  extern __shared__ uint8_t sm[];
+  extern __shared__ __align__(16) uint8_t smbuf[];
   if (misc->flags) return;
   const uint64_t rpos = misc->rpos;
   const uint64_t Ls = wstart - rpos;
   const uint64_t cs = (uint64_t)blockIdx.x * C;
   if (cs >= Ls) return;
   const uint32_t have = (uint32_t)(Ls - cs < (uint64_t)C + kEntries + 64 ? Ls - cs : (uint64_t)C + kEntries + 64);
-  for (uint32_t i = threadIdx.x; i < have; i += blockDim.x) sm[i] = c[rpos + cs + i];
-  __syncthreads();
+  const uint8_t *sm = stage_bytes(smbuf, c + rpos + cs, have);
   if (threadIdx.x != 0) return;
   uint32_t p = chunk[2 * blockIdx.x];
   uint64_t idx = chunk[2 * blockIdx.x + 1];
@@ -527,7 +538,7 @@ int run_parse(const dm::Head &h, const dm::Layout &L, const uint8_t *buf, uint64
   const uint32_t gb = (uint32_t)std::max<uint64_t>(1, ceil_div(std::max<uint64_t>(h.P, 32), 256));
   dm::k_global<<<gb, 256, 0, s>>>(ga, offset, maxg, reinterpret_cast<uint32_t *>(ws + L.finals), misc, st);
   if (h.P) {
-    const size_t stage = L.chunk_bytes + dm::kEntries + 64;
+    const size_t stage = L.chunk_bytes + dm::kEntries + 64 + 32;
     // dynamic shared memory beyond 48 KB (per device: set on every call, it is cheap)
     if (cudaFuncSetAttribute(dm::k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(dm::k_write, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024) != cudaSuccess ||

@@ -138,3 +138,15 @@ def test_device_combine_config4_65536_to_2048_256_16():
     for t in (2048, 256, 16):
         got = R.recoil_device_combine(c, d_in, t).cpu().numpy()
         assert np.array_equal(got, R.recoil_combine_splits(c, t)), t
+
+
+def test_device_parse_config5_split_density():
+    """~150 000 splits (config 5's 8-GPU density over 2^27 symbols is 85 248 / 64; here denser):
+    ~12 MB of split records, parse chunks larger than the minimum, every byte decoded."""
+    sym, c = _enc("image", 1 << 27, 150_000)
+    assert R.recoil_inspect(c)["n_splits"] > 140_000  # the encoder may find fewer points (S:275)
+    rc, _, out = _device_decode(c)
+    assert rc == 0 and np.array_equal(out, sym)
+    d_in = torch.from_numpy(c).cuda()
+    got = R.recoil_device_combine(c, d_in, 10_000).cpu().numpy()
+    assert np.array_equal(got, R.recoil_combine_splits(c, 10_000))
