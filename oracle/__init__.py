@@ -21,7 +21,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _HDR = os.path.join(_HERE, "oracle.h")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# ORACLE_SANITIZE=1: an ASan + UBSan build (tools/sanitize_host.sh) under its own name
+_SAN = os.environ.get("ORACLE_SANITIZE") == "1"
+_LIB = os.path.join(_HERE, "liboracle_san.so" if _SAN else "liboracle.so")
 _lib = None
 
 L = 1 << 16
@@ -38,7 +40,9 @@ class OracleError(RuntimeError):
 def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", _SRC, "-o", _LIB])
+        san = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined"] if _SAN \
+            else []
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", *san, _SRC, "-o", _LIB])
     return _LIB
 
 

@@ -64,5 +64,30 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_sanitized() -> str:
+    """Host library objects with ASan + UBSan (SURVEY §4 "Sanitizers"), linked with the regular
+    CUDA kernel objects into librecoil_san.so (tools/sanitize_host.sh loads it through RECOIL_LIB)."""
+    build()
+    host, cuda, headers = _sources()
+    out_dir = os.path.join(PKG, "build_san")
+    os.makedirs(out_dir, exist_ok=True)
+    san = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined", "-O1", "-g"]
+    objs = []
+    for src in host:
+        obj = os.path.join(out_dir, os.path.basename(src) + ".o")
+        if _stale(obj, [src] + headers):
+            subprocess.check_call(["g++", *CXXFLAGS, *san, "-c", src, "-o", obj])
+        objs.append(obj)
+    objs += [os.path.join(BUILD, os.path.basename(src) + ".o") for src in cuda]
+    lib = os.path.join(PKG, "librecoil_san.so")
+    cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    subprocess.check_call(["g++", "-shared", *san, "-o", lib, *objs, f"-L{cuda_lib}", "-lcudart", "-lpthread", "-ldl",
+                           f"-Wl,-rpath,{cuda_lib}"])
+    return lib
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--sanitize" in sys.argv:
+        print(build_sanitized())
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))
