@@ -500,3 +500,40 @@ def test_overhead_bands_vs_paper(lam):
     small = oracle.combine(large, 16)
     assert len(small) - base <= 2500
     assert (oracle.recoil_decode(small) == sym).all()
+
+
+def test_oracle_fuzz_1000_instances():
+    """SPEC's acceptance fuzz: 1 000 random instances with W <= 8 lanes, M <= 9
+    splits, N <= 512 symbols, 1 <= n <= 16 and random models (incl. one-symbol and skewed
+    ones).  Each: the container round-trips through the serial decode (stack property,
+    P:124), every split task decodes exactly its committed range correctly (P:303-315,
+    reading Z13), and combining to every smaller split count decodes identically."""
+    rng = np.random.default_rng(20261017)
+    for it in range(1000):
+        W = int(rng.integers(1, 9))
+        n = int(rng.integers(1, 17))
+        N = int(rng.integers(0, 513))
+        M = int(rng.integers(1, 10))
+        k = int(rng.integers(1, min(256, 1 << n) + 1))
+        pmf = np.zeros(256)
+        syms_present = rng.choice(256, size=k, replace=False)
+        pmf[syms_present] = rng.random(k) ** int(rng.integers(1, 6)) + 1e-9
+        sym = rng.choice(256, size=N, p=pmf / pmf.sum()).astype(np.uint8)
+        hist = synth.histogram(sym) if N else np.bincount(syms_present, minlength=256).astype(np.uint64)
+        if (hist > 0).sum() > (1 << n):
+            continue
+        f = oracle.build_model(hist, n)
+        c = oracle.recoil_encode(sym, f, n, M, W)
+        assert (oracle.recoil_decode(c) == sym).all(), it
+        info = oracle.container_info(c)
+        out = np.zeros(max(N, 1), np.uint8)
+        for t in range(info["M"]):
+            if N == 0:
+                break
+            out2, lo, hi = oracle.recoil_decode_task(c, t, np.zeros(max(N, 1), np.uint8))
+            assert (out2[lo:hi + 1] == sym[lo:hi + 1]).all(), (it, t)
+            out[lo:hi + 1] = out2[lo:hi + 1]
+        assert N == 0 or (out[:N] == sym).all(), it
+        for target in range(1, info["M"]):
+            cc = oracle.combine(c, target)
+            assert (oracle.recoil_decode(cc) == sym).all(), (it, target)
