@@ -433,14 +433,30 @@ def main():
             c_enc = R.recoil_encode(sym, f, 11, per_gpu_splits * world)
         enc_s = time.perf_counter() - t0
         if world > 1:
-            c_enc.tofile(share)
+            try:
+                c_enc.tofile(share)
+            except OSError as e:  # no room for a file: hand the container over through the process group
+                log(f"container file hand-off failed ({e}); broadcasting over gloo")
+                share = None
     if world > 1:
-        pg.barrier()
-        if rank != 0:
-            c_enc = np.fromfile(share, dtype=np.uint8)
-        pg.barrier()
-        if rank == 0:
-            os.unlink(share)
+        # the hand-off path (or its failure) is decided by rank 0 and broadcast with the length
+        import torch
+        meta = torch.tensor([len(c_enc) if rank == 0 else 0, 1 if (rank == 0 and share) else 0], dtype=torch.int64)
+        pg.broadcast(meta, 0)
+        n_c, by_file = int(meta[0]), bool(meta[1])
+        if by_file:
+            pg.barrier()
+            if rank != 0:
+                c_enc = np.fromfile(share, dtype=np.uint8)
+            pg.barrier()
+            if rank == 0:
+                os.unlink(share)
+        else:
+            buf = torch.from_numpy(c_enc) if rank == 0 else torch.empty(n_c, dtype=torch.uint8)
+            step = 256 << 20
+            for o in range(0, n_c, step):
+                pg.broadcast(buf[o:o + step], 0)
+            c_enc = buf.numpy()
     M_enc = R.recoil_inspect(c_enc)["n_splits"]
     # decoder-adaptive scalability: shrink the metadata to this job's parallelism
     target = per_gpu_splits * world
