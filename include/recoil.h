@@ -194,6 +194,14 @@ int recoil_decoder_create_subset(const uint8_t *container, uint64_t len, uint32_
  * for n_runs = 0 or a run of 0 splits. */
 int recoil_decoder_create_grouped(const uint8_t *container, uint64_t len, uint32_t n_runs,
                                   const uint32_t *run_tasks, const uint32_t *run_splits, recoil_decoder **out);
+/* Decoder-adaptive scalability in one call: the whole stream planned for the
+ * parallelism of `device` -- when the container holds more split points than
+ * waves_x100 / 100 waves of the decode kernel's resident warps (0: 150, the measured
+ * best), the decode uses the points recoil_combine_splits would keep for
+ * that count (in place, nothing rewritten); else all of them.  Errors as
+ * recoil_decoder_create, E_CUDA (occupancy query). */
+int recoil_decoder_create_for_device(const uint8_t *container, uint64_t len, int device, uint32_t waves_x100,
+                                     recoil_decoder **out);
 int recoil_decoder_plan(const recoil_decoder *dec, recoil_plan *plan);
 
 /* Asynchronous host->device copy on cuda_stream of the packed LUT and task

@@ -369,42 +369,114 @@ extern "C" int recoil_decoder_create(const uint8_t *container, uint64_t len, uin
   }
 }
 
+namespace recoil {
+namespace {
+
+// Parse for a decoder-side combine: the full parse (host-expanded task records, the default
+// GPU plan) for static containers, the light parse (fused plan) for adaptive ones.
+int parse_for_subset(const uint8_t *container, uint64_t len, std::shared_ptr<Container> *out) {
+  auto full = std::make_shared<Container>();
+  const bool adaptive = container && len >= 4 && std::memcmp(container, "RCA1", 4) == 0;
+  int rc = parse_container(container, len, full.get(), /*light=*/adaptive);
+  if (rc) return rc;
+  if (full->partitioned) return RECOIL_E_ARG;  // partitions cannot be combined
+  *out = std::move(full);
+  return RECOIL_OK;
+}
+
+// The container viewed with only the split points `keep` (ascending point indices): the
+// decode runs through the dropped points.  Full parse: the kept points' anchors,
+// differences and spans; light parse: their record offsets (rec_off[j + 1] bounds kept record
+// j's bytes: the next kept record, a looser but valid bound; the last bound is the last kept
+// record's end).
+std::shared_ptr<Container> select_points(const Container &full, const std::vector<uint64_t> &keep) {
+  auto view = std::make_shared<Container>(full);
+  const uint32_t W = full.W;
+  view->offset.clear();
+  view->maxg.clear();
+  view->rec_off.clear();
+  view->state.clear();
+  view->gdiff.clear();
+  view->sync_start.clear();
+  view->bidx.clear();
+  for (uint64_t k : keep) {
+    view->offset.push_back(full.offset[k]);
+    view->maxg.push_back(full.maxg[k]);
+    if (full.light) {
+      view->rec_off.push_back(full.rec_off[k]);
+    } else {
+      view->state.insert(view->state.end(), full.state.begin() + k * W, full.state.begin() + (k + 1) * W);
+      view->gdiff.insert(view->gdiff.end(), full.gdiff.begin() + k * W, full.gdiff.begin() + (k + 1) * W);
+      view->sync_start.push_back(full.sync_start[k]);
+      view->bidx.push_back(full.bidx[k]);
+    }
+  }
+  if (full.light) view->rec_off.push_back(keep.empty() ? full.rec_off[0] : full.rec_off[keep.back() + 1]);
+  view->M = (uint32_t)keep.size() + 1;
+  return view;
+}
+
+int finish_decoder(std::shared_ptr<const Container> view, uint64_t tb, uint64_t te, recoil_decoder **out) {
+  Decoder *d = new Decoder();
+  int rc = build_decoder_from(std::move(view), tb, te, d, true);
+  if (rc) {
+    delete d;
+    return rc;
+  }
+  *out = reinterpret_cast<recoil_decoder *>(d);
+  return RECOIL_OK;
+}
+
+// the split points recoil_combine_splits(c, target) keeps: 1-based positions k, 2k, ...
+std::vector<uint64_t> combine_keep(const Container &c, uint32_t target) {
+  std::vector<uint64_t> keep;
+  const uint64_t P = c.M - 1;
+  if (target >= c.M) {
+    for (uint64_t k = 0; k < P; ++k) keep.push_back(k);
+  } else {
+    const uint64_t step = ceil_div(c.M, target);
+    for (uint64_t pos = step; pos <= P; pos += step) keep.push_back(pos - 1);
+  }
+  return keep;
+}
+
+}  // namespace
+}  // namespace recoil
+
 extern "C" int recoil_decoder_create_subset(const uint8_t *container, uint64_t len, uint32_t target_splits,
                                             uint64_t task_begin, uint64_t task_end, recoil_decoder **out) {
   if (!container || !out || target_splits < 1) return RECOIL_E_ARG;
   *out = nullptr;
   try {
-    auto full = std::make_shared<Container>();
-    int rc = parse_container(container, len, full.get(), /*light=*/true);
+    std::shared_ptr<Container> full;
+    int rc = parse_for_subset(container, len, &full);
     if (rc) return rc;
-    if (full->partitioned) return RECOIL_E_ARG;  // partitions cannot be combined
-    // the view: the split points recoil_combine_splits would keep (1-based positions
-    // k, 2k, ... with k = ceil(M / target), Z11/Z12), over the same container bytes
-    auto view = std::make_shared<Container>(*full);
-    if (target_splits < full->M) {
-      const uint64_t P = full->M - 1, k = ceil_div(full->M, target_splits);
-      view->offset.clear();
-      view->maxg.clear();
-      view->rec_off.clear();
-      for (uint64_t pos = k; pos <= P; pos += k) {
-        view->offset.push_back(full->offset[pos - 1]);
-        view->maxg.push_back(full->maxg[pos - 1]);
-        view->rec_off.push_back(full->rec_off[pos - 1]);
-      }
-      view->M = (uint32_t)view->offset.size() + 1;
-      // rec_off[k + 1] bounds record k's bytes (here: the next kept record, a
-      // looser but valid bound); the last bound is the last kept record's end
-      const uint64_t last = view->offset.empty() ? 0 : (P / k) * k;
-      view->rec_off.push_back(view->offset.empty() ? full->rec_off[0] : full->rec_off[last]);
+    return finish_decoder(select_points(*full, combine_keep(*full, target_splits)), task_begin, task_end, out);
+  } catch (const std::bad_alloc &) {
+    return RECOIL_E_NOMEM;
+  }
+}
+
+extern "C" int recoil_decoder_create_for_device(const uint8_t *container, uint64_t len, int device, uint32_t waves_x100,
+                                                recoil_decoder **out) {
+  if (!container || !out || len < 8) return RECOIL_E_ARG;
+  *out = nullptr;
+  try {
+    std::shared_ptr<Container> full;
+    int rc = parse_for_subset(container, len, &full);
+    if (rc) return rc;
+    int warps = 0, sms = 0;
+    if (full->adaptive) {
+      uint64_t e = 0;
+      for (uint32_t k = 0; k < full->K; ++k) e += full->mlen[k];
+      rc = recoil_decode_occupancy_adaptive(device, full->K, e, &warps, &sms);
+    } else {
+      rc = recoil_decode_occupancy(device, full->n, &warps, &sms);
     }
-    Decoder *d = new Decoder();
-    rc = build_decoder_from(view, task_begin, task_end, d, true);
-    if (rc) {
-      delete d;
-      return rc;
-    }
-    *out = reinterpret_cast<recoil_decoder *>(d);
-    return RECOIL_OK;
+    if (rc) return rc;
+    const uint64_t target = std::max<uint64_t>(1, (uint64_t)warps * sms * (waves_x100 ? waves_x100 : 150) / 100);
+    return finish_decoder(select_points(*full, combine_keep(*full, (uint32_t)std::min<uint64_t>(target, full->M))),
+                          0, UINT64_MAX, out);
   } catch (const std::bad_alloc &) {
     return RECOIL_E_NOMEM;
   }
@@ -416,46 +488,24 @@ extern "C" int recoil_decoder_create_grouped(const uint8_t *container, uint64_t 
   if (!container || !out || n_runs < 1 || !run_tasks || !run_splits) return RECOIL_E_ARG;
   *out = nullptr;
   try {
-    auto full = std::make_shared<Container>();
-    int rc = parse_container(container, len, full.get(), /*light=*/true);
+    std::shared_ptr<Container> full;
+    int rc = parse_for_subset(container, len, &full);
     if (rc) return rc;
-    if (full->partitioned) return RECOIL_E_ARG;  // partitions cannot be combined
     for (uint32_t r = 0; r < n_runs; ++r)
       if (run_splits[r] == 0) return RECOIL_E_ARG;
-    // task i spans run_splits[r] consecutive encoder splits (segments) for the
-    // run r it falls in; the point after its last segment is kept, every other
-    // point is dropped (the decode runs through it); the last task
-    // takes the segments that remain
-    auto view = std::make_shared<Container>(*full);
+    // task i spans run_splits[r] consecutive encoder splits (segments) for the run r it
+    // falls in; the point after its last segment is kept, every other point is dropped
+    // (the decode runs through it); the last task takes the segments that remain
     const uint64_t P = full->M - 1;
-    view->offset.clear();
-    view->maxg.clear();
-    view->rec_off.clear();
-    uint64_t seg = 0, last = 0;
-    bool any = false;
+    std::vector<uint64_t> keep;
+    uint64_t seg = 0;
     for (uint32_t r = 0; r < n_runs; ++r)
       for (uint32_t i = 0; i < run_tasks[r]; ++i) {
         seg += run_splits[r];
         if (seg > P) break;
-        const uint64_t k = seg - 1;  // point k closes segment k
-        view->offset.push_back(full->offset[k]);
-        view->maxg.push_back(full->maxg[k]);
-        view->rec_off.push_back(full->rec_off[k]);
-        last = k;
-        any = true;
+        keep.push_back(seg - 1);  // point k closes segment k
       }
-    view->M = (uint32_t)view->offset.size() + 1;
-    // rec_off[j + 1] bounds kept record j's bytes (the next kept record: a looser
-    // but valid bound); the last bound is the last kept record's end
-    view->rec_off.push_back(any ? full->rec_off[last + 1] : full->rec_off[0]);
-    Decoder *d = new Decoder();
-    rc = build_decoder_from(view, 0, UINT64_MAX, d, true);
-    if (rc) {
-      delete d;
-      return rc;
-    }
-    *out = reinterpret_cast<recoil_decoder *>(d);
-    return RECOIL_OK;
+    return finish_decoder(select_points(*full, keep), 0, UINT64_MAX, out);
   } catch (const std::bad_alloc &) {
     return RECOIL_E_NOMEM;
   }

@@ -35,7 +35,7 @@ EXPORTS = [
     "recoil_pipeline_create", "recoil_pipeline_device_bytes", "recoil_pipeline_run", "recoil_pipeline_status",
     "recoil_pipeline_launches", "recoil_pipeline_destroy", "recoil_quantize", "recoil_encode_adaptive",
     "recoil_decode_adaptive", "recoil_decode_occupancy_adaptive", "recoil_decoder_create_subset",
-    "recoil_decoder_create_grouped", "recoil_pipeline_run_at", "recoil_pipeline_span", "recoil_multi_plan",
+    "recoil_decoder_create_grouped", "recoil_decoder_create_for_device", "recoil_pipeline_run_at", "recoil_pipeline_span", "recoil_multi_plan",
     "recoil_multi_decode", "recoil_multi_nccl_available", "recoil_device_decoder_create",
     "recoil_device_decoder_plan", "recoil_device_upload", "recoil_device_decode", "recoil_device_decoder_status",
     "recoil_device_decoder_launches", "recoil_device_decoder_destroy", "recoil_device_combine_plan",
@@ -123,6 +123,7 @@ def load(path: str = LIB_PATH):
         "recoil_decoder_create_subset": (i32, [P, u64, u32, u64, u64, P]),
         "recoil_decoder_create_grouped": (i32, [P, u64, u32, P, P, P]),
         "recoil_pipeline_run_at": (i32, [P, P, P, u64, P, u32]),
+        "recoil_decoder_create_for_device": (i32, [P, u64, i32, u32, P]),
         "recoil_pipeline_span": (i32, [P, P, P]),
         "recoil_multi_plan": (i32, [P, u64, u32, P]),
         "recoil_multi_decode": (i32, [P, u64, u32, P, P, i32, P, P]),
@@ -277,6 +278,14 @@ def recoil_decoder_create_subset(container, target_splits: int, task_begin: int 
     return h
 
 
+def recoil_decoder_create_for_device(container, device: int = 0, waves_x100: int = 0) -> ctypes.c_void_p:
+    c = _u8(container)
+    h = ctypes.c_void_p()
+    _check(load().recoil_decoder_create_for_device(c.ctypes.data, c.size, device, waves_x100, ctypes.byref(h)),
+           "recoil_decoder_create_for_device")
+    return h
+
+
 def recoil_decoder_create_grouped(container, run_tasks, run_splits) -> ctypes.c_void_p:
     """Tasks in stream order: run_tasks[r] tasks of run_splits[r] encoder splits each, the last task
     takes the rest."""
@@ -359,11 +368,13 @@ class GpuDecoder:
     """
 
     def __init__(self, container, device: int = 0, task_begin: int = 0, task_end: int = (1 << 64) - 1,
-                 stream=None, subset: int | None = None, grouped=None):
+                 stream=None, subset: int | None = None, grouped=None, for_device: bool = False):
         import torch
         self.container = _u8(container)
         self.device = torch.device("cuda", device)
-        if grouped is not None:  # (run_tasks, run_splits): recoil_decoder_create_grouped
+        if for_device:  # decoder-adaptive: combine in place to this GPU's parallelism
+            self.handle = recoil_decoder_create_for_device(self.container, device)
+        elif grouped is not None:  # (run_tasks, run_splits): recoil_decoder_create_grouped
             self.handle = recoil_decoder_create_grouped(self.container, *grouped)
         else:
             self.handle = (recoil_decoder_create(self.container, task_begin, task_end) if subset is None else

@@ -539,3 +539,26 @@ def test_one_task_longer_than_2pow31_symbols():
         dec.close()
         assert np.array_equal(out, sym)
         del out
+
+
+def test_decoder_create_for_device_combines_to_the_gpu():
+    """recoil_decoder_create_for_device (decoder-adaptive scalability): a container
+    with 3 waves of split points is decoded with 1.5 waves of tasks (the points
+    recoil_combine_splits keeps), bit-exact; a container with fewer points keeps all of them."""
+    warps, sms = R.recoil_decode_occupancy(0, 11)
+    sym = synth.text_bytes(40 << 20, 5)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 3 * warps * sms)
+    dec = R.GpuDecoder(c, 0, for_device=True)
+    assert dec.plan["n_tasks"] == R.recoil_inspect(R.recoil_combine_splits(c, warps * sms * 3 // 2))["n_splits"]
+    dec.upload()
+    dec.decode()
+    assert dec.status()[0] == 0 and (dec.output().cpu().numpy() == sym).all()
+    dec.close()
+    small = R.recoil_encode(sym, f, 11, 100)
+    dec = R.GpuDecoder(small, 0, for_device=True)
+    assert dec.plan["n_tasks"] == 100
+    dec.upload()
+    dec.decode()
+    assert dec.status()[0] == 0 and (dec.output().cpu().numpy() == sym).all()
+    dec.close()
