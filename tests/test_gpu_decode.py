@@ -483,30 +483,32 @@ def _move_max_group(c, k, delta):
 def test_crafted_record_cannot_write_outside_the_plan():
     """a middle split point whose max group is moved 2000 groups up (still
     < G, so the light parse accepts it) must not make its task write past the plan's output
-    window: the kernel checks every task's window against [out_base, out_base + out_count)
-    and flags E_INCONSISTENT.  Guard bytes on both sides of d_out stay untouched."""
+    window.  The host-expanded plans reject it at create (full parse: sync starts no longer
+    increasing); the light-parse e2e pipeline decodes it with the in-kernel window check
+    (E_INCONSISTENT); the on-device metadata path flags it on the GPU and leaves guard bytes
+    on both sides of d_out untouched."""
     sym = synth.exp_bytes(2_000_000, 50, 4)
     f = R.recoil_build_model(synth.histogram(sym), 11)
     c = R.recoil_encode(sym, f, 11, 512)
     assert bytes(_move_max_group(c, 105, 0)) == bytes(c)  # the re-serialiser is exact
     bad = _move_max_group(c, 105, 2000)  # point 105 = the entry of task 105, inside the plan [100, 110)
-    # the default plan parses every record on the host (full parse) and rejects the container
-    with pytest.raises(R.RecoilError) as ei:
-        R.GpuDecoder(bad, 0, 100, 110)
-    assert ei.value.rc == R.RECOIL_E_INCONSISTENT
-    # the light-parse plans (decoder-side subset, e2e pipeline chunks) expand the records in the
-    # kernel: there the kernel's window check must catch it
-    dec = R.GpuDecoder(bad, 0, 100, 110, subset=512)
+    # the host-expanded plans parse every record (full parse) and reject the container
+    for kw in ({}, {"subset": 512}, {"for_device": True}):
+        with pytest.raises(R.RecoilError) as ei:
+            R.GpuDecoder(bad, 0, 100, 110, **kw) if "for_device" not in kw else R.GpuDecoder(bad, 0, **kw)
+        assert ei.value.rc == R.RECOIL_E_INCONSISTENT
     guard = 1 << 20
     assert 2000 * 32 < guard
-    big = torch.full((dec.plan["out_count"] + 2 * guard,), 0xAB, dtype=torch.uint8, device="cuda")
-    dec.upload()
-    dec.decode(out=big[guard:guard + dec.plan["out_count"]])
-    rc, _ = dec.status()
-    dec.close()
-    assert R.ERRORS.get(rc) == "RECOIL_E_INCONSISTENT"
-    host = big.cpu().numpy()
-    assert (host[:guard] == 0xAB).all() and (host[-guard:] == 0xAB).all()
+    # the e2e pipeline plans from the light parse and expands the records in the kernel: there the
+    # kernel's window check must catch it (status E_INCONSISTENT, no fault)
+    pinned = torch.empty(len(bad), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = bad
+    pipe = R.HostPipeline(pinned.numpy(), 0, n_chunks=2, n_streams=2, task_begin=100, task_end=110)
+    lo, hi = pipe.span()
+    host = torch.zeros(hi - lo, dtype=torch.uint8, pin_memory=True)
+    pipe.run(host, lo)
+    assert R.ERRORS.get(pipe.status()[0]) == "RECOIL_E_INCONSISTENT"
+    pipe.close()
     # the on-device metadata path checks the sync starts on the GPU and skips the tasks
     dd = R.DeviceContainerDecoder(bad, 0)
     big = torch.full((dd.plan["out_count"] + 2 * guard,), 0xAB, dtype=torch.uint8, device="cuda")
