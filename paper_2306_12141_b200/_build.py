@@ -64,6 +64,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_c_client() -> str:
+    """examples/c_client.c: the C ABI from plain C (gcc, linked against librecoil.so and cudart)."""
+    build()
+    src = os.path.join(ROOT, "examples", "c_client.c")
+    exe = os.path.join(ROOT, "examples", "c_client")
+    if _stale(exe, [src, LIB, os.path.join(INCLUDE, "recoil.h")]):
+        cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", f"-I{INCLUDE}", f"-I{CUDA_INC}", src,
+                               "-o", exe, f"-L{PKG}", "-lrecoil", f"-Wl,-rpath,{PKG}", f"-L{cuda_lib}", "-lcudart",
+                               f"-Wl,-rpath,{cuda_lib}"])
+    return exe
+
+
 def build_sanitized() -> str:
     """Host library objects with ASan + UBSan (SURVEY §4 "Sanitizers"), linked with the regular
     CUDA kernel objects into librecoil_san.so (tools/sanitize_host.sh loads it through RECOIL_LIB)."""
