@@ -625,6 +625,22 @@ def main():
                            "GB/s_into_root": round((N_total - n_rank) / float(t.item()) / 1e9, 2), "bit_exact": gok,
                            "backend": "nccl", "note": "rank spans -> rank 0, batched point-to-point; not in value"}
         del full
+    if rank == 0 and world == 1 and target < M_enc:
+        # the same combine on the GPU (recoil_device_combine, NEXT 2): the encoded container already
+        # in device memory shrunk to this job's split count; output byte-identical to the host combine
+        d_enc = torch.from_numpy(c_enc).to(dev)
+        dts = []
+        for i in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            d_small = R.recoil_device_combine(c_enc, d_enc, target)
+            dts.append(time.perf_counter() - t0)
+        same = bool(d_small.numel() == len(c) and torch.equal(d_small, torch.from_numpy(c).to(dev)))
+        extra["device_combine"] = {"ms": round(1e3 * float(np.median(dts)), 3), "host_combine_ms": round(1e3 * combine_s, 3),
+                                   "from_splits": int(M_enc), "to_splits": int(M), "byte_identical": same,
+                                   "note": "recoil_device_combine wall time (two 8-byte read-backs, the word "
+                                           "stream copied device to device) vs recoil_combine_splits on the host"}
+        del d_enc, d_small
     if rank == 0 and world == 1 and not args.no_extra:
         # the paper's comparison: conventional partitioned decoder at the same count,
         # alternating with Recoil in one run (median of --reps repetitions of K steps each)
