@@ -311,14 +311,15 @@ void recoil_pipeline_destroy(recoil_pipeline *p);
 /* ---------------------------------------------------------------------- */
 
 /* The client copies the received container to the GPU unchanged; the split
- * metadata is decoded there (global series, split-record offsets, LUT, task
- * heads) and the decode kernel reads the records in place.  The host reads
- * only the fixed header and the model block.  Whole stream, "RCL1" only. */
+ * metadata is decoded there (global series, split-record offsets by a
+ * speculative chunked parse, LUT, the 192-B task records of every split task)
+ * and the decode kernel streams those records.  The host reads only the fixed
+ * header and the model block.  Whole stream, "RCL1" only. */
 typedef struct recoil_device_decoder recoil_device_decoder;
 typedef struct {
   uint64_t container_offset; /* copy the container to d_buffer + container_offset (puts its words 512-B aligned) */
   uint64_t buffer_bytes;     /* d_buffer size: offset + container + zeroed word padding (>= 256 words + 256 B) */
-  uint64_t workspace_bytes;  /* d_workspace size (status, parse results, LUT, task heads) */
+  uint64_t workspace_bytes;  /* d_workspace size (status, parse results, LUT, task records) */
   uint64_t out_count;        /* d_out bytes (N rounded up to 16) */
   uint64_t n_symbols;        /* N */
   uint32_t n_tasks;          /* split tasks (M; 0 for N = 0) */
@@ -340,8 +341,9 @@ int recoil_device_upload(const recoil_device_decoder *dec, const uint8_t *contai
 /* Stream-ordered: the metadata kernels, then the decode kernel, writing the N
  * symbols to d_out[0, N) (it may write d_out up to out_count).  Metadata that
  * fails its checks (offsets out of range or not increasing, record list not
- * ending at the words, widths out of range) sets E_INCONSISTENT in the status
- * word and no task decodes.  Errors: E_ARG, E_CUDA. */
+ * ending at the words, widths out of range, a group difference above its anchor
+ * group, a boundary past N, sync starts not increasing) sets E_INCONSISTENT in
+ * the status word and the affected tasks do not decode.  Errors: E_ARG, E_CUDA. */
 int recoil_device_decode(recoil_device_decoder *dec, void *d_buffer, void *d_workspace, uint8_t *d_out,
                          void *cuda_stream);
 /* As recoil_decoder_status for the last recoil_device_decode. */
