@@ -108,3 +108,12 @@ def test_pipeline_into_a_span_sized_host_buffer():
         with pytest.raises(R.RecoilError):
             pipe.run(host, lo + 1)  # the span starts before host_first
         pipe.close()
+
+
+def test_multi_decode_more_devices_than_tasks():
+    sym, c = _stream(20_000, 3, "exp")
+    assert R.recoil_inspect(c)["n_splits"] <= 3
+    plans, outs, gat, rc, ms = _run(c, [0] * 8, 0)
+    assert rc == 0
+    assert sum(p["n_tasks"] for p in plans) == R.recoil_inspect(c)["n_splits"]
+    assert (gat.cpu().numpy() == sym).all()
