@@ -182,19 +182,25 @@ def make_stream(cfg: str, n_total: int, lam_override: float = 0.0, start: int = 
                           start=start)
 
 
+# warp-instructions per 32-symbol group in the n = 11 kernel's unrolled steady state
+# (cuobjdump -sass)
+STEADY_INSTR_PER_GROUP = 19
+
+
 def issue_roofline(prof: dict, avg_ms: float, clocks, sms: int, groups: int):
     """The other binding resource: warp-instruction issue (plain integer ALU path, no tensor cores).
     Peak = 4 schedulers x 1 warp-instruction per cycle per SM x SMs x the SM clock sampled during the run
     (B200_PROFILING.md unit counts).  'achieved' counts the algorithmic instructions: the steady-state
-    20 warp-instructions per 32-symbol group (SASS of the unrolled block) x the launch's
+    STEADY_INSTR_PER_GROUP warp-instructions per 32-symbol group (SASS of the unrolled block) x the launch's
     groups; 'measured' is ncu's smsp__inst_executed of the same launch (all overheads included)."""
     if avg_ms <= 0:
         return None
     mhz = (clocks.report() or {}).get("sm_mhz") or 1965.0
     peak = 4 * sms * mhz * 1e6
-    alg = 20 * groups / (avg_ms / 1e3)
+    alg = STEADY_INSTR_PER_GROUP * groups / (avg_ms / 1e3)
     out = {"bound": "alu", "achieved": round(alg / 1e9, 1), "peak": round(peak / 1e9, 1),
-           "unit": "G warp-instructions/s", "frac": round(alg / peak, 4), "instructions_per_group": 20}
+           "unit": "G warp-instructions/s", "frac": round(alg / peak, 4),
+           "instructions_per_group": STEADY_INSTR_PER_GROUP}
     inst = prof.get("warp_instructions_per_launch")
     if inst:
         out["measured"] = round(inst / (avg_ms / 1e3) / 1e9, 1)

@@ -7,7 +7,8 @@
 // (32 symbols, one per lane), top-down:
 //   refill  (Eq. 4): lanes with x < L read one 16-bit word, in
 //           decreasing lane order: m = ballot(x < L), lane j reads
-//           word[cursor - popc(m & lanes_above_j)], cursor -= popc(m);
+//           word[cursor + 1 - popc(m & lanes_at_or_above_j)], cursor -= the
+//           warp maximum of that count (REDUX.MAX: lane 0's count = popc(m));
 //   decode  (Eq. 2): e = lut[x mod 2^n] from the shared-memory
 //           packed LUT (s | bias << 8 | f << 20), x = f (x >> n) + bias.
 // Synchronization Phase: a lane is initialised with its 16-bit
@@ -189,9 +190,9 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ uint32_t lanemask_gt() {
+__device__ __forceinline__ uint32_t lanemask_ge() {
   uint32_t m;
-  asm("mov.u32 %0, %%lanemask_gt;" : "=r"(m));
+  asm("mov.u32 %0, %%lanemask_ge;" : "=r"(m));
   return m;
 }
 
@@ -240,14 +241,16 @@ struct Warp {
   // model tables (coarse bucket -> entry range, entries F | (f-1) << 16,
   // per-model value offset), n, the coarse shift and the largest model id
   uint32_t mid32, coarse32, ent32, delta32, nb, cshift, kmax;
-  uint32_t gt;       // lanes above this one
+  uint32_t ge;       // this lane and the lanes above it
   int lane;
-  // 2 x (slice-relative index of the next word to read), unsigned: slices hold
-  // < 2^31 words, so the doubled index needs all 32 bits (a signed form
+  // 2 x (1 + slice-relative index of the next word to read), unsigned: slices
+  // hold < 2^31 words, so the doubled index needs all 32 bits (a signed form
   // overflowed for slices of >= 2^30 words: the 8 GiB config 5 stream in one
-  // launch); the only negative cursor of a valid stream is the end state -1
+  // launch); the end state (next word -1) is cursor2 = 0.  The +1 lets a lane
+  // address its word as cursor2 - 2 pge with pge counting the needing lanes at
+  // or above it (see refill).
   uint32_t cursor2;
-  int cchunk;        // cursor2 >> 9 at the last window check
+  int cchunk;        // (cursor2 - 2) >> 9 at the last window check
 
   // a7: warp-cooperative prefetch of word chunk c (256 words = 32 lanes x 16 B)
   __device__ __forceinline__ void issue_chunk(int c) {
@@ -260,7 +263,7 @@ struct Warp {
   // 4-chunk ring).  16 groups consume at most 512 words (two chunks), so one
   // check covers a whole output block.
   __device__ __forceinline__ void window_check() {
-    const int c = (int)(cursor2 >> 9);
+    const int c = (int)((cursor2 - 2u) >> 9);
     if (c != cchunk) {
       __syncwarp();  // all lanes' reads of the slot being refilled (chunk c+1's) are done
       do {
@@ -272,15 +275,16 @@ struct Warp {
     }
   }
   // Eq. 4 with the interleaved read order: lanes below read after the
-  // lanes above them.  pre = needing lanes above this one (POPC); the warp total
-  // comes from REDUX, which runs outside the LDS/POPC pipe.
+  // lanes above them.  pge = needing lanes at or above this one (POPC), so a
+  // needing lane reads word cursor - pge + 1; the warp's word count is lane 0's
+  // pge, i.e. the maximum, taken by REDUX (which runs outside the LDS/POPC pipe;
+  // one instruction fewer per group than a REDUX.SUM of the need flags).
   __device__ __forceinline__ uint32_t refill(uint32_t x) {
     const bool need = x < kL;
     const uint32_t m = __ballot_sync(kFull, need);
-    const int pre = __popc(m & gt);
-    const int step2 = __reduce_add_sync(kFull, need ? -2 : 0);  // -2 x (words this group)
-    const uint32_t w = lds_u16(ring32 | ((cursor2 + (uint32_t)(pre * p->neg2)) & (kRingBytes - 2)));
-    cursor2 += (uint32_t)step2;
+    const uint32_t pge = __popc(m & ge);
+    const uint32_t w = lds_u16(ring32 | ((cursor2 + pge * (uint32_t)p->neg2) & (kRingBytes - 2)));
+    cursor2 -= 2u * __reduce_max_sync(kFull, pge);
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   const int warp = threadIdx.x >> 5;
   w.ring32 = smem_addr(smem_dyn + L::kRing + warp * 2 * kRingWords);
   w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
-  w.gt = lanemask_gt();
+  w.ge = lanemask_ge();
   w.lut32 = smem_addr(sm_lut);
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   }
   // a7: the task's word window: chunks c, c-1, c-2 resident, c-3 in flight
   auto issue_window = [&](int32_t cursor0) {
-    w.cursor2 = 2u * (uint32_t)cursor0;
+    w.cursor2 = 2u * (uint32_t)cursor0 + 2u;
     w.cchunk = cursor0 >> 8;
     w.issue_chunk(w.cchunk);
     w.issue_chunk(w.cchunk - 1);
@@ -763,10 +767,10 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     // every initialised lane back at L.
     // the cursor as a signed slice index: -1 is the codec's end state; anything
     // else at or beyond the slice end is an underflow (the slice has < 2^31 words)
-    const uint32_t cur_u = w.cursor2 >> 1;
-    const int cursor = w.cursor2 == 0xFFFFFFFEu ? -1 : (int)cur_u;
+    const uint32_t cur_u = (w.cursor2 - 2u) >> 1;
+    const int cursor = w.cursor2 == 0u ? -1 : (int)cur_u;
     bool bad_end = false;
-    const bool under = w.cursor2 != 0xFFFFFFFEu && cur_u >= (uint32_t)p.n_chunks * kChunkWords;
+    const bool under = w.cursor2 != 0u && cur_u >= (uint32_t)p.n_chunks * kChunkWords;
     if (end_cursor != kNoEndCheck) {
       const bool lane_ok = (init_group < lo_group) || x == kL;
       bad_end = (cursor != (int)end_cursor) || !__all_sync(kFull, lane_ok);

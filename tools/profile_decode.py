@@ -7,14 +7,14 @@ from paper_2306_12141_b200 import recoil as R
 cfg = sys.argv[1] if len(sys.argv) > 1 else "config2"
 kind = sys.argv[2] if len(sys.argv) > 2 else "recoil"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-waves = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+waves = float(sys.argv[4]) if len(sys.argv) > 4 else 0
 warps, sms = R.recoil_decode_occupancy(0, 11)
 if cfg == "config2":
-    sym = synth.text_bytes(100 << 20, synth.seed_for(2)); M = warps * sms * (waves or 3)
+    sym = synth.text_bytes(100 << 20, synth.seed_for(2)); M = int(warps * sms * (waves or 3))
 elif cfg == "config1":
     sym = synth.exp_bytes(1 << 20, 50, synth.seed_for(1, 50)); M = 16
 else:
-    sym = synth.exp_bytes(1 << 30, 50, synth.seed_for(3, 50)); M = warps * sms * (waves or 8)
+    sym = synth.exp_bytes(1 << 30, 50, synth.seed_for(3, 50)); M = int(warps * sms * (waves or 8))
 f = R.recoil_build_model(synth.histogram(sym), 11)
 c = R.recoil_encode(sym, f, 11, M) if kind == "recoil" else R.recoil_partitioned_encode(sym, f, 11, M)
 dec = R.GpuDecoder(c, 0); dec.upload()
