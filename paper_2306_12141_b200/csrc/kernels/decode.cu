@@ -284,7 +284,7 @@ struct Warp {
     const uint32_t m = __ballot_sync(kFull, need);
     const uint32_t pge = __popc(m & ge);
     const uint32_t w = lds_u16(ring32 | ((cursor2 + pge * (uint32_t)p->neg2) & (kRingBytes - 2)));
-    cursor2 -= 2u * __reduce_max_sync(kFull, pge);
+    cursor2 += __reduce_max_sync(kFull, pge) * (uint32_t)p->neg2;  // IMAD: FMA pipe, not ALU
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
@@ -345,6 +345,15 @@ struct Warp {
       if (S == 2) stg_v4(dst + 32 * lane + 16, lds_v4(a + 16));
     }
     __syncwarp();  // the staging block is rewritten by the next group steps
+  }
+  // a whole block inside the write window; dst = this lane's 16 S bytes of it
+  template <int S>
+  __device__ __forceinline__ void flush_whole(uint8_t *dst) {
+    __syncwarp();
+    const uint32_t a = stage32 + (16 * S - S) * lane;
+    stg_v4(dst, lds_v4(a));
+    if (S == 2) stg_v4(dst + 16, lds_v4(a + 16));
+    __syncwarp();
   }
   template <int S>
   __device__ __forceinline__ void flush(uint8_t *dst, uint32_t rel, uint32_t woff, uint32_t wend) {
@@ -731,24 +740,34 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       // three blocks before the end
       int rel = (g >> 4) - b_lo;
       const int full_lo = ((lo_group & 15) == 0) ? 0 : 1;
-      uint8_t *dst = out_blo + (uint32_t)rel * kBlk;
-      uint32_t c = (uint32_t)rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part, block-relative
+      // Every whole block lies inside the write window [woff, wend): block full_lo
+      // starts at or above woff, and the top one ends at or below wend because the
+      // sync start bounding whi is >= 32 min_init and these blocks are
+      // below group min_init.  Checked once here (records that break it are
+      // inconsistent), so the whole-block flushes need no per-chunk test.
+      const bool whole_ok = (uint32_t)(rel + 1) * kBlk <= wend;
+      if (!whole_ok) {
+        if (lane == 0) {
+          atomicOr(&p.status->flags, 4u);
+          atomicMax(&p.status->bad_task, 0xFFFFFFFFu - task_id);
+        }
+        rel = full_lo - 1;
+      }
+      uint8_t *dst = out_blo + (uint32_t)rel * kBlk + 16 * S * lane;  // this lane's 16 S-byte part
       for (; rel >= full_lo + 3; --rel) {
         stage_block(b_lo + rel);
         x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
+        w.template flush_whole<S>(dst);
         dst -= kBlk;
-        c -= kBlk;
       }
       for (; rel >= full_lo; --rel) {
         next_task_step();
         stage_block(b_lo + rel);
         x = run_block<NB>(w, lut, sym, x);
-        w.template flush_at<S>(dst, c, woff, wend);
+        w.template flush_whole<S>(dst);
         dst -= kBlk;
-        c -= kBlk;
       }
-      if (full_lo) {  // tail: the partial block of lo_group
+      if (full_lo && whole_ok) {  // tail: the partial block of lo_group
         stage_block(b_lo);
         x = run_part<NB, false>(w, lut, sym, x, b_lo * 16 + 15, lo_group, 0, 0);
         w.template flush<S>(out_blo, 0, woff, wend);

@@ -17,6 +17,9 @@ WORKLOADS = [  # (name, kind, size, lam, splits)
     ("exp50_1G_10656", "exp", 1 << 30, 50, 10656),
     ("image_1G_10656", "image", 1 << 30, 0, 10656),
     ("text100M_21312", "text", 100 << 20, 0, 21312),
+    ("text100M_10656", "text", 100 << 20, 0, 10656),
+    ("text100M_14208", "text", 100 << 20, 0, 14208),
+    ("exp50_1G_21312", "exp", 1 << 30, 50, 21312),
 ]
 if os.environ.get("AB_WORKLOADS"):
     WORKLOADS = [w for w in WORKLOADS if w[0] in os.environ["AB_WORKLOADS"].split(",")]
