@@ -333,6 +333,22 @@ typedef struct {
  * a word stream of >= 2^31 words), E_NOMEM. */
 int recoil_device_decoder_create(const uint8_t *head, uint64_t head_len, uint64_t container_len,
                                  recoil_device_decoder **out);
+/* The split tasks [task_begin, task_end) only (a multi-GPU shard: the tasks
+ * are independent; task_end = UINT64_MAX: to the last task).  Every split record is
+ * still parsed on the device (the series and record offsets are a list), the task
+ * records and the decode cover the range; the output keeps absolute symbol indices
+ * (d_out holds out_count = N rounded up to 16 bytes; the range writes its committed
+ * span, recoil_device_decoder_span, plus at most the 16-B chunks around it, whose
+ * bytes are the stream's own).  Errors: as recoil_device_decoder_create, E_ARG for an
+ * empty or out-of-range task range. */
+int recoil_device_decoder_create_range(const uint8_t *head, uint64_t head_len, uint64_t container_len,
+                                       uint64_t task_begin, uint64_t task_end, recoil_device_decoder **out);
+/* After recoil_device_decode (synchronises the stream: two 8-byte read-backs of the
+ * device task records): the committed symbol span [*out_lo, *out_hi) of the
+ * decoder's task range (sync start of the point before the range .. sync start of
+ * its last point, Z13; the whole [0, N) for the full range).  Errors: E_ARG, E_CUDA. */
+int recoil_device_decoder_span(const recoil_device_decoder *dec, const void *d_workspace, void *cuda_stream,
+                               uint64_t *out_lo, uint64_t *out_hi);
 int recoil_device_decoder_plan(const recoil_device_decoder *dec, recoil_device_plan *plan);
 /* Convenience H2D (stream-ordered): container -> d_buffer + container_offset, and the
  * zero padding after it.  A caller that copies the container itself must zero

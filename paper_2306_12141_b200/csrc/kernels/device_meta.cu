@@ -272,12 +272,13 @@ __device__ __forceinline__ bool point_of(const uint8_t *c, uint64_t rec, uint32_
   return __any_sync(0xFFFFFFFFu, bad) || bidx >= (int64_t)N;
 }
 
-__global__ void k_taskrecs(uint64_t M, uint64_t N, uint64_t B, uint64_t G, const uint8_t *c, const uint64_t *offset,
-                           const uint32_t *maxg, const uint64_t *rec_off, Misc *misc, DeviceStatus *st,
-                           TaskRec *tasks) {
-  const uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// tasks [tb, te) of the container; record t - tb holds task t (task_id t)
+__global__ void k_taskrecs(uint64_t M, uint64_t tb, uint64_t te, uint64_t N, uint64_t B, uint64_t G, const uint8_t *c,
+                           const uint64_t *offset, const uint32_t *maxg, const uint64_t *rec_off, Misc *misc,
+                           DeviceStatus *st, TaskRec *tasks) {
+  const uint64_t t = tb + (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const uint32_t lane = threadIdx.x & 31;
-  if (t >= M) return;
+  if (t >= te) return;
   const uint64_t P = M - 1;
   TaskRec r;
   bool bad = misc->flags != 0;
@@ -316,9 +317,9 @@ __global__ void k_taskrecs(uint64_t M, uint64_t N, uint64_t B, uint64_t G, const
     r.end_cursor = kNoEndCheck;
   }
   // lane j stores lanes[j]; lane 0 the scalar fields (16-B aligned record)
-  tasks[t].lanes[lane] = r.lanes[lane];
+  tasks[t - tb].lanes[lane] = r.lanes[lane];
   if (lane == 0) {
-    TaskRec &o = tasks[t];
+    TaskRec &o = tasks[t - tb];
     o.cursor0 = r.cursor0;
     o.end_cursor = r.end_cursor;
     o.commit_lo = r.commit_lo;
@@ -558,8 +559,9 @@ int run_parse(const dm::Head &h, const dm::Layout &L, const uint8_t *buf, uint64
 
 using namespace recoil;
 
-extern "C" int recoil_device_decoder_create(const uint8_t *head, uint64_t head_len, uint64_t container_len,
-                                            recoil_device_decoder **out) {
+extern "C" int recoil_device_decoder_create_range(const uint8_t *head, uint64_t head_len, uint64_t container_len,
+                                                  uint64_t task_begin, uint64_t task_end,
+                                                  recoil_device_decoder **out) {
   if (!out) return RECOIL_E_ARG;
   *out = nullptr;
   try {
@@ -583,7 +585,14 @@ extern "C" int recoil_device_decoder_create(const uint8_t *head, uint64_t head_l
     }
     dd->words_pad = 2 * (word_count - h.B) + 256;
     dd->buf_bytes = dd->coff + container_len + dd->words_pad;
-    // the decode plan: the whole stream, task records built on the device
+    // the decode plan: tasks [tb, te) (the whole stream by default), task records built
+    // on the device; the output is addressed by absolute symbol index (out_base 0)
+    const uint64_t M = h.N ? h.M : 0;
+    const uint64_t tb = task_begin, te = task_end == ~0ull ? M : task_end;
+    if (tb > te || te > M || (M && tb == te)) {
+      delete dd;
+      return RECOIL_E_ARG;
+    }
     auto c = std::make_shared<Container>();
     c->n = h.n;
     c->W = kLanes;
@@ -606,9 +615,9 @@ extern "C" int recoil_device_decoder_create(const uint8_t *head, uint64_t head_l
     if (present != 1) d.single_symbol = -1;
     recoil_plan &p = d.plan;
     std::memset(&p, 0, sizeof(p));
-    p.task_begin = 0;
-    p.task_end = h.M;
-    p.n_tasks = h.N ? h.M : 0;
+    p.task_begin = tb;
+    p.task_end = te;
+    p.n_tasks = (uint32_t)(te - tb);
     p.prob_bits = h.n;
     p.word_lo = 0;
     p.word_count = word_count;
@@ -630,6 +639,31 @@ extern "C" int recoil_device_decoder_create(const uint8_t *head, uint64_t head_l
   } catch (const std::bad_alloc &) {
     return RECOIL_E_NOMEM;
   }
+}
+
+extern "C" int recoil_device_decoder_create(const uint8_t *head, uint64_t head_len, uint64_t container_len,
+                                            recoil_device_decoder **out) {
+  return recoil_device_decoder_create_range(head, head_len, container_len, 0, ~0ull, out);
+}
+
+extern "C" int recoil_device_decoder_span(const recoil_device_decoder *dec, const void *d_workspace, void *stream,
+                                          uint64_t *out_lo, uint64_t *out_hi) {
+  if (!dec || !d_workspace || !out_lo || !out_hi) return RECOIL_E_ARG;
+  const DeviceDecoder *dd = reinterpret_cast<const DeviceDecoder *>(dec);
+  const recoil_plan &p = dd->dec.plan;
+  *out_lo = *out_hi = 0;
+  if (!p.n_tasks) return RECOIL_OK;
+  // the committed range of the first and the last task of the range (device task records)
+  const TaskRec *recs = reinterpret_cast<const TaskRec *>(static_cast<const char *>(d_workspace) + dd->L.heads);
+  uint64_t lo = 0, hi = 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(&lo, &recs[0].commit_lo, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(&hi, &recs[p.n_tasks - 1].commit_hi, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RECOIL_E_CUDA;
+  *out_lo = lo;
+  *out_hi = hi + 1;
+  return RECOIL_OK;
 }
 
 extern "C" int recoil_device_decoder_plan(const recoil_device_decoder *dec, recoil_device_plan *plan) {
@@ -670,8 +704,9 @@ extern "C" int recoil_device_decode(recoil_device_decoder *dec, void *d_buffer, 
   if (rc) return rc;
   if (!h.N) return RECOIL_OK;
   dm::k_lut<<<1, 256, 0, s>>>(buf + dd->coff, h.model_pos, h.count, h.n, reinterpret_cast<uint8_t *>(ws + dd->L.lut));
-  const uint32_t hb = (uint32_t)ceil_div(32 * h.M, 256);
-  dm::k_taskrecs<<<hb, 256, 0, s>>>(h.M, h.N, h.B, h.G, buf + dd->coff,
+  const recoil_plan &pl = dd->dec.plan;
+  const uint32_t hb = (uint32_t)ceil_div(32 * (uint64_t)pl.n_tasks, 256);
+  dm::k_taskrecs<<<hb, 256, 0, s>>>(h.M, pl.task_begin, pl.task_end, h.N, h.B, h.G, buf + dd->coff,
                                     reinterpret_cast<const uint64_t *>(ws + dd->L.offset),
                                     reinterpret_cast<const uint32_t *>(ws + dd->L.maxg),
                                     reinterpret_cast<const uint64_t *>(ws + dd->L.rec_off),

@@ -39,7 +39,7 @@ EXPORTS = [
     "recoil_multi_decode", "recoil_multi_nccl_available", "recoil_device_decoder_create",
     "recoil_device_decoder_plan", "recoil_device_upload", "recoil_device_decode", "recoil_device_decoder_status",
     "recoil_device_decoder_launches", "recoil_device_decoder_destroy", "recoil_device_combine_plan",
-    "recoil_device_combine",
+    "recoil_device_combine", "recoil_device_decoder_create_range", "recoil_device_decoder_span",
 ]
 
 
@@ -129,6 +129,8 @@ def load(path: str = LIB_PATH):
         "recoil_multi_decode": (i32, [P, u64, u32, P, P, i32, P, P]),
         "recoil_multi_nccl_available": (i32, []),
         "recoil_device_decoder_create": (i32, [P, u64, u64, P]),
+        "recoil_device_decoder_create_range": (i32, [P, u64, u64, u64, u64, P]),
+        "recoil_device_decoder_span": (i32, [P, P, P, P, P]),
         "recoil_device_decoder_plan": (i32, [P, P]),
         "recoil_device_upload": (i32, [P, P, P, P]),
         "recoil_device_decode": (i32, [P, P, P, P, P]),
@@ -555,14 +557,15 @@ class DeviceContainerDecoder:
     copied to the GPU unchanged and its split metadata decoded there (global series, record
     offsets, LUT, task heads), then the decode kernel runs.  Device buffers are torch tensors."""
 
-    def __init__(self, container, device: int = 0, stream=None):
+    def __init__(self, container, device: int = 0, stream=None, task_begin: int = 0, task_end: int | None = None):
         import torch
         c = _u8(container)
         self.container = c
         self.device = torch.device("cuda", device)
         h = ctypes.c_void_p()
-        _check(load().recoil_device_decoder_create(c.ctypes.data, c.size, c.size, ctypes.byref(h)),
-               "recoil_device_decoder_create")
+        te = (1 << 64) - 1 if task_end is None else task_end
+        _check(load().recoil_device_decoder_create_range(c.ctypes.data, c.size, c.size, task_begin, te,
+                                                         ctypes.byref(h)), "recoil_device_decoder_create_range")
         self.handle = h
         pl = recoil_device_plan()
         _check(load().recoil_device_decoder_plan(h, ctypes.byref(pl)), "recoil_device_decoder_plan")
@@ -591,6 +594,13 @@ class DeviceContainerDecoder:
 
     def output(self):
         return self.out[:self.plan["n_symbols"]]
+
+    def span(self) -> tuple[int, int]:
+        """The committed symbol span [lo, hi) of this decoder's task range (after decode)."""
+        lo, hi = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _check(load().recoil_device_decoder_span(self.handle, self.workspace.data_ptr(), self.stream.cuda_stream,
+                                                 ctypes.byref(lo), ctypes.byref(hi)), "recoil_device_decoder_span")
+        return lo.value, hi.value
 
     def launches(self) -> int:
         return _check(load().recoil_device_decoder_launches(self.handle), "recoil_device_decoder_launches")

@@ -150,3 +150,49 @@ def test_device_parse_config5_split_density():
     d_in = torch.from_numpy(c).cuda()
     got = R.recoil_device_combine(c, d_in, 10_000).cpu().numpy()
     assert np.array_equal(got, R.recoil_combine_splits(c, 10_000))
+
+
+@pytest.mark.parametrize("kind,n,M,shards", [("text", 3_000_017, 700, 5), ("image", 2_000_000, 20000, 3),
+                                             ("exp", 1 << 20, 16, 16), ("exp", 100_000, 2, 2)])
+def test_device_task_ranges_shard_the_stream(kind, n, M, shards):
+    """recoil_device_decoder_create_range (a multi-GPU shard on the device path): each
+    range's committed span equals the host shard plan's, the spans tile [0, N), and every
+    span's bytes equal the input (and the oracle's decode)."""
+    sym, c = _enc(kind, n, M)
+    bounds = R.recoil_shard_plan(c, shards)
+    want = oracle.recoil_decode(c.tobytes()) if n <= 3_000_017 else sym
+    assert np.array_equal(want, sym)
+    prev_hi = 0
+    for tb, te in zip(bounds[:-1], bounds[1:]):
+        if tb == te:
+            continue
+        dd = R.DeviceContainerDecoder(c, 0, task_begin=tb, task_end=te)
+        assert dd.plan["n_tasks"] == te - tb
+        dd.upload()
+        dd.decode()
+        rc, bad = dd.status()
+        assert rc == 0, (R.ERRORS.get(rc), bad)
+        lo, hi = dd.span()
+        host = R.GpuDecoder(c, 0, tb, te)
+        assert (lo, hi) == (host.plan["out_lo"], host.plan["out_hi"])
+        host.close()
+        assert lo == prev_hi
+        prev_hi = hi
+        out = dd.output().cpu().numpy()
+        dd.close()
+        assert np.array_equal(out[lo:hi], sym[lo:hi])
+    assert prev_hi == n
+
+
+def test_device_task_range_single_tasks_and_edges():
+    """One-task ranges at the first, a middle and the last task."""
+    sym, c = _enc("text", 500_000, 40)
+    for tb in (0, 17, 39):
+        dd = R.DeviceContainerDecoder(c, 0, task_begin=tb, task_end=tb + 1)
+        dd.upload()
+        dd.decode()
+        assert dd.status()[0] == 0
+        lo, hi = dd.span()
+        assert lo < hi and (tb > 0 or lo == 0) and (tb < 39 or hi == len(sym))
+        assert np.array_equal(dd.output().cpu().numpy()[lo:hi], sym[lo:hi])
+        dd.close()

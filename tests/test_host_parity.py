@@ -420,3 +420,22 @@ def test_multi_plan_equals_shard_plan_and_decoder_plans():
         assert lo == len(sym)
     with pytest.raises(R.RecoilError):
         R.recoil_multi_plan(c, 0)
+
+
+def test_device_range_decoder_arguments():
+    """recoil_device_decoder_create_range checks the range on the host (no GPU call)."""
+    import ctypes
+    sym = synth.text_bytes(200_000, 3)
+    f = R.recoil_build_model(synth.histogram(sym), 11)
+    c = R.recoil_encode(sym, f, 11, 10)
+    lib = R.load()
+    for tb, te, ok in [(0, 10, True), (3, 7, True), (9, 10, True), (0, (1 << 64) - 1, True), (5, 5, False),
+                       (6, 5, False), (0, 11, False), (10, 11, False)]:
+        h = ctypes.c_void_p()
+        rc = lib.recoil_device_decoder_create_range(c.ctypes.data, c.size, c.size, tb, te, ctypes.byref(h))
+        assert (rc == 0) == ok, (tb, te, rc)
+        if rc == 0:
+            pl = R.recoil_device_plan()
+            assert lib.recoil_device_decoder_plan(h, ctypes.byref(pl)) == 0
+            assert pl.n_tasks == (10 if te > 10 else te) - tb
+            lib.recoil_device_decoder_destroy(h)
