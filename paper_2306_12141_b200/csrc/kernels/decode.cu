@@ -10,7 +10,8 @@
 //           word[cursor + 1 - popc(m & lanes_at_or_above_j)], cursor -= the
 //           warp maximum of that count (REDUX.MAX: lane 0's count = popc(m));
 //   decode  (Eq. 2): e = lut[x mod 2^n] from the shared-memory
-//           packed LUT (s | bias << 8 | f << 20), x = f (x >> n) + bias.
+//           packed LUT (s | bias << 8 | f << 20; n <= 11: four
+//           bank-interleaved copies, one per 8 lanes), x = f (x >> n) + bias.
 // Synchronization Phase: a lane is initialised with its 16-bit
 // anchor state in its anchor group, immediately before its first read;
 // uninitialised lanes hold 0xFFFFFFFF (never < L, so they never read) and
@@ -115,25 +116,32 @@ struct Params {
 // Shared memory per block (dynamic; about 31 KB for n = 11 at 8 warps): the word
 // rings need 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
 constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
+// n <= 11: the packed LUT in kLutCopies = 4 interleaved copies (entry i of copy c at
+// word 4 i + c, so copy c sits in banks c, c + 4, ..., c + 28) and lanes 8c .. 8c + 7
+// read copy c: a random gather of 32 slots then spreads over the banks as 4 groups
+// of 8 lanes on 8 banks each (3.27 wavefronts on average instead of 3.49 for one
+// copy; 32 KB at n = 11, still two 24-warp CTAs per SM).  The decode is bound by the
+// l1tex data pipe at ~5.8 wavefronts per 32-symbol group.
+constexpr int kLutCopies = 4, kCopyMaxBits = 11;
 template <int NB>
 __host__ __device__ constexpr int lut_words() {
-  return NB <= 0 ? 128 * warps_per_block<NB>() : NB <= 9 ? 512 : NB <= 12 ? (1 << NB) : 512;
+  return NB <= 0 ? 128 * warps_per_block<NB>()
+                 : NB <= kCopyMaxBits ? ((kLutCopies << NB) > 512 ? (kLutCopies << NB) : 512)
+                                      : NB <= 12 ? (1 << NB) : 512;
 }
-// bytes before the LUT: staging + records, padded to 7 KB mod 8 KB (see Smem)
+// bytes before the LUT: staging + records
 constexpr int kPreLut(int W, int S) { return W * ((int)kBlockBytes * S + 2 * (int)sizeof(TaskRec)); }
-// padding that puts the LUT at 1 KB + pre + pad = 0 mod A (A = 8 KB for the LOP3-addressed
-// LUT of n <= 11, else 2 KB so the rings after the LUT stay 2 KB-aligned)
+// padding that puts the LUT at 1 KB + pre + pad = 0 mod A (A = 2 KB)
 constexpr int kLutPad(int W, int S, int A) { return ((A - 1024 - kPreLut(W, S) % A) % A + A) % A; }
-// Block layout (byte offsets into the dynamic shared memory).  Order matters: the
-// CTA's shared memory starts 1 KB into its shared window (the reserved system
-// area), so stage + rec + pad (7 KB mod 8 KB) put the LUT on an 8 KB boundary,
-// and a LUT of <= 8 KB (n <= 11) is addressed with one LOP3: base | ((x << 2) &
-// mask).  The LUT is at least 2 KB, so the word rings after it start 2 KB-aligned
-// (ring addresses are base | (pos & 0x7FE)).  Both alignments are checked at
-// kernel start.
+// Block layout (byte offsets into the dynamic shared memory).  The CTA's shared
+// memory starts 1 KB into its shared window (the reserved system area); stage + rec
+// + pad put the LUT on a 2 KB boundary and the LUT is a multiple of 2 KB, so the
+// word rings after it start 2 KB-aligned (ring addresses are base | (pos & 0x7FE);
+// checked at kernel start).
 //   stage[W][512 S]  per warp 512 symbols of output staging
 //   rec[W][2]        current / next task record (prebuilt-record plans)
-//   lut[lut_words]   n <= 12: packed LUT s | bias << 8 | f << 20; n >= 13
+//   lut[lut_words]   n <= 12: packed LUT s | bias << 8 | f << 20 (4 copies for
+//                    n <= 11, see kLutCopies); n >= 13
 //                    (NEXT row 1): f and F per symbol (the 2^n slot -> symbol bytes
 //                    follow the layout); adaptive: each warp's staged model ids
 //   ring[W][1024]    per warp 2 KB word window (u16)
@@ -143,11 +151,10 @@ struct Smem {
   static constexpr int W = warps_per_block<NB>();
   static constexpr int kStage = 0;
   static constexpr int kRec = kStage + W * (int)kBlockBytes * S;
-  static constexpr int kLut = kRec + W * 2 * (int)sizeof(TaskRec) + kLutPad(W, S, NB >= 1 && NB <= 11 ? 8192 : 2048);
+  static constexpr int kLut = kRec + W * 2 * (int)sizeof(TaskRec) + kLutPad(W, S, 2048);
   static constexpr int kRing = kLut + 4 * lut_words<NB>();
   static constexpr int kBytes = kRing + W * 2 * kRingWords;
 };
-constexpr int kOrLutMaxBits = 11;  // LUT base alignment trick up to 8 KB
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
@@ -317,8 +324,16 @@ struct Warp {
       sts_u16(stage32 + k * 64, lo + lds_u32(delta32 + 4 * km));
       return ((e >> 16) + 1) * (x >> nb) + slot - (e & 0xFFFFu);  // f (x >> n) + slot - F
     } else if constexpr (NB <= kNarrowMaxBits) {
-      const uint32_t e = NB <= kOrLutMaxBits ? lds_u32(lut32 | ((x << 2) & ((4u << NB) - 4)))
-                                             : lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
+      uint32_t e;
+      if constexpr (NB <= kCopyMaxBits) {
+        // entry slot of this lane's copy: lut32 + 16 slot as one IMAD (FMA pipe; inline PTX
+        // so ptxas keeps the multiply-add instead of a shift + add on the ALU pipe)
+        uint32_t a;
+        asm("mad.lo.u32 %0, %1, 16, %2;" : "=r"(a) : "r"(x & ((1u << NB) - 1)), "r"(lut32));
+        e = lds_u32(a);
+      } else {
+        e = lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
+      }
       sts_u8(stage32 + k * 32, e);
       // f (x >> n) + bias as f ((x >> n) - 2^12) + (e >> 8), since e >> 8 = bias + 2^12 f
       // (mod 2^32; the true result is < 2^32): LEA.HI + SHF + SHF + IMAD
@@ -472,7 +487,12 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       reinterpret_cast<uint32_t *>(sym_dyn)[i] = reinterpret_cast<const uint32_t *>(p.lut)[i];
   } else if constexpr (NB <= kNarrowMaxBits) {
     constexpr uint32_t kWords = 1u << NB;
-    if (kWords >= 4) {
+    if constexpr (NB <= kCopyMaxBits) {  // kLutCopies = 4 copies, interleaved by entry
+      for (uint32_t i = threadIdx.x; i < kWords; i += kThreads) {
+        const uint32_t v = reinterpret_cast<const uint32_t *>(p.lut)[i];
+        reinterpret_cast<uint4 *>(sm_lut)[i] = make_uint4(v, v, v, v);
+      }
+    } else if (kWords >= 4) {
       for (uint32_t i = threadIdx.x; i < kWords / 4; i += kThreads)
         reinterpret_cast<int4 *>(sm_lut)[i] = reinterpret_cast<const int4 *>(p.lut)[i];
     } else if (threadIdx.x < kWords) {
@@ -495,6 +515,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
   w.ge = lanemask_ge();
   w.lut32 = smem_addr(sm_lut);
+  if constexpr (NB >= 1 && NB <= kCopyMaxBits) w.lut32 += 4 * (lane >> 3);  // this lane's LUT copy
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
@@ -504,7 +525,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     w.cshift = p.nbits > p.ad_cbits ? p.nbits - p.ad_cbits : 0;
     w.kmax = p.ad_K - 1;
   }
-  if ((NB >= 1 && NB <= kOrLutMaxBits && (w.lut32 & ((4u << NB) - 1))) || (w.ring32 & (kRingBytes - 1))) {
+  if (w.ring32 & (kRingBytes - 1)) {
     // shared-memory layout assumption broken: fail loudly
     if (threadIdx.x == 0) atomicOr(&p.status->flags, 4u);
     return;
