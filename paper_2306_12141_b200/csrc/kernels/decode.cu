@@ -113,7 +113,7 @@ struct Params {
   uint32_t ad_K, ad_E, nbits, ad_cbits, ad_crow;  // + coarse bucket bits, u16 row length
 };
 
-// Shared memory per block (dynamic; about 31 KB for n = 11 at 8 warps): the word
+// Shared memory per block (dynamic; about 101 KB for n = 11 at 24 warps): the word
 // rings need 2 KB alignment (ring addresses are formed with one LOP3: base | (pos & 0x7FE)).
 constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 // n <= 11: the packed LUT in kLutCopies = 4 interleaved copies (entry i of copy c at
@@ -123,6 +123,7 @@ constexpr int kNarrowMaxBits = 12;  // packed u32 LUT up to n = 12
 // copy; 32 KB at n = 11, still two 24-warp CTAs per SM).  The decode is bound by the
 // l1tex data pipe at ~5.8 wavefronts per 32-symbol group.
 constexpr int kLutCopies = 4, kCopyMaxBits = 11;
+static_assert(kLutCopies % 4 == 0 && 32 % kLutCopies == 0, "copies are staged as uint4 and split the warp evenly");
 template <int NB>
 __host__ __device__ constexpr int lut_words() {
   return NB <= 0 ? 128 * warps_per_block<NB>()
@@ -326,10 +327,10 @@ struct Warp {
     } else if constexpr (NB <= kNarrowMaxBits) {
       uint32_t e;
       if constexpr (NB <= kCopyMaxBits) {
-        // entry slot of this lane's copy: lut32 + 16 slot as one IMAD (FMA pipe; inline PTX
-        // so ptxas keeps the multiply-add instead of a shift + add on the ALU pipe)
+        // entry slot of this lane's copy: lut32 + 4 kLutCopies slot as one IMAD (FMA pipe;
+        // inline PTX so ptxas keeps the multiply-add instead of a shift + add on the ALU pipe)
         uint32_t a;
-        asm("mad.lo.u32 %0, %1, 16, %2;" : "=r"(a) : "r"(x & ((1u << NB) - 1)), "r"(lut32));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(x & ((1u << NB) - 1)), "n"(4 * kLutCopies), "r"(lut32));
         e = lds_u32(a);
       } else {
         e = lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
@@ -487,10 +488,12 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
       reinterpret_cast<uint32_t *>(sym_dyn)[i] = reinterpret_cast<const uint32_t *>(p.lut)[i];
   } else if constexpr (NB <= kNarrowMaxBits) {
     constexpr uint32_t kWords = 1u << NB;
-    if constexpr (NB <= kCopyMaxBits) {  // kLutCopies = 4 copies, interleaved by entry
+    if constexpr (NB <= kCopyMaxBits) {  // kLutCopies copies, interleaved by entry
       for (uint32_t i = threadIdx.x; i < kWords; i += kThreads) {
         const uint32_t v = reinterpret_cast<const uint32_t *>(p.lut)[i];
-        reinterpret_cast<uint4 *>(sm_lut)[i] = make_uint4(v, v, v, v);
+#pragma unroll
+        for (int c = 0; c < kLutCopies / 4; ++c)
+          reinterpret_cast<uint4 *>(sm_lut)[kLutCopies / 4 * i + c] = make_uint4(v, v, v, v);
       }
     } else if (kWords >= 4) {
       for (uint32_t i = threadIdx.x; i < kWords / 4; i += kThreads)
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
   w.ge = lanemask_ge();
   w.lut32 = smem_addr(sm_lut);
-  if constexpr (NB >= 1 && NB <= kCopyMaxBits) w.lut32 += 4 * (lane >> 3);  // this lane's LUT copy
+  if constexpr (NB >= 1 && NB <= kCopyMaxBits) w.lut32 += 4 * (lane / (32 / kLutCopies));  // this lane's copy
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
     w.coarse32 = smem_addr(sym_dyn);
