@@ -27,11 +27,11 @@
 // loaded one block before a task starts and expanded in the kernel (row a1),
 // prebuilt records (partitioned containers) stream in by cp.async; tasks are
 // handed out by an atomic counter (persistent warps, 2 CTAs of 24 warps per
-// SM).  Output: in whole 16-group blocks of the static codec (n <= 12) each group's
-// 32 symbol bytes go straight to HBM as one warp store (a full 32-B sector per
-// warp: no staging wavefronts, measured +2 % over staging); the
-// partial blocks at a task's edges and the adaptive codec stage a 512-symbol block
-// in shared memory and write each lane's 16 S bytes with 16-byte stores inside the
+// SM).  Output: in whole 16-group blocks of the static codec (n <= 12) and the
+// adaptive codec each group's 32 symbols go straight to HBM as one warp store (full
+// 32-B sectors: no staging wavefronts, measured +2 % over staging);
+// the partial blocks at a task's edges (and n >= 13) stage a 512-symbol block in
+// shared memory and write each lane's 16 S bytes with 16-byte stores inside the
 // task's write window.  All shared accesses use 32-bit shared-window addresses
 // (inline PTX) computed once per warp.
 #include <cuda_runtime.h>
@@ -191,6 +191,9 @@ __device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ void stg_u16(void *p, uint32_t v) {
+  asm volatile("st.global.u16 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void stg_u8(void *p, uint32_t v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -303,7 +306,7 @@ struct Warp {
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
-  uint8_t *outp = nullptr;  // whole blocks: this lane's byte of the output block (symbols go straight to HBM)
+  uint8_t *outp = nullptr;  // whole blocks: this lane's symbol (S bytes) of group 0 of the output block
   template <int NB, bool DIRECT = false>
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
     if constexpr (NB <= 0) {
@@ -330,7 +333,10 @@ struct Warp {
         }
       }
       const uint32_t e = lds_u32(ent32 + 4 * lo);
-      sts_u16(stage32 + k * 64, lo + lds_u32(delta32 + 4 * km));
+      if constexpr (DIRECT)  // whole blocks: straight to HBM (64 B = two full sectors per warp)
+        stg_u16(outp + k * 64, lo + lds_u32(delta32 + 4 * km));
+      else
+        sts_u16(stage32 + k * 64, lo + lds_u32(delta32 + 4 * km));
       return ((e >> 16) + 1) * (x >> nb) + slot - (e & 0xFFFFu);  // f (x >> n) + slot - F
     } else if constexpr (NB <= kNarrowMaxBits) {
       uint32_t e;
@@ -446,7 +452,8 @@ __device__ __forceinline__ uint32_t run_part(Warp &w, const uint32_t *lut, const
 #endif
 constexpr int kAdUnroll = RECOIL_AD_UNROLL;
 // A whole 16-group block with every lane initialised: no branch per group.  The static
-// codec (n <= 12) stores each group's symbols directly to w.outp (set by the caller).
+// codec (n <= 12) and the adaptive codec store each group's symbols directly to w.outp
+// (set by the caller).
 template <int NB>
 __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, const uint8_t *sym, uint32_t x) {
   w.window_check();
@@ -456,7 +463,7 @@ __device__ __forceinline__ uint32_t run_block(Warp &w, const uint32_t *lut, cons
 #pragma unroll kAdUnroll
     for (int k = 15; k >= 0; --k) {
       x = w.refill(x);
-      x = w.decode<NB>(lut, sym, x, k);
+      x = w.template decode<NB, true>(lut, sym, x, k);
     }
   } else {
 #pragma unroll
@@ -789,7 +796,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
         }
         rel = full_lo - 1;
       }
-      constexpr bool kDirect = NB >= 1 && NB <= kNarrowMaxBits;
+      constexpr bool kDirect = NB <= kNarrowMaxBits;  // static n <= 12 and the adaptive codec
       uint8_t *dst = out_blo + (uint32_t)rel * kBlk + (kDirect ? S : 16 * S) * lane;  // this lane's part
       for (; rel >= full_lo + 3; --rel) {
         stage_block(b_lo + rel);
