@@ -6,11 +6,11 @@ import numpy as np, torch, synth
 from paper_2306_12141_b200 import recoil as R
 kind = sys.argv[1] if len(sys.argv) > 1 else "text"
 mib = int(sys.argv[2]) if len(sys.argv) > 2 else 100
-waves = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+waves = float(sys.argv[3]) if len(sys.argv) > 3 else 1
 warps, sms = R.recoil_decode_occupancy(0, 11)
 sym = synth.text_bytes(mib << 20, synth.seed_for(2)) if kind == "text" else synth.exp_bytes(mib << 20, 50, synth.seed_for(3, 50))
 f = R.recoil_build_model(synth.histogram(sym), 11)
-c = R.recoil_encode(sym, f, 11, warps * sms * waves)
+c = R.recoil_encode(sym, f, 11, int(warps * sms * waves))
 M = R.recoil_inspect(c)["n_splits"]
 dec = R.GpuDecoder(c, 0); dec.upload()
 lib = R.load()
