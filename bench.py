@@ -307,12 +307,14 @@ def run_reference(args, rank, world):
 # our arm
 # ------------------------------------------------------------------------------------------
 
-def adaptive_extra(args, local, stream, timed_decode, peak):
+def adaptive_extra(args, local, stream, timed_decode, peak, log2n: int = 25):
     """NEXT rows 1 + 4: the adaptive codec (index-keyed Gaussian models, 16-bit symbols, n = 16) on the
-    latent workload, 2^25 symbols, one split per resident warp."""
+    latent workload, 2^log2n symbols (2^25: ~15 div2k-sized latents; 2^27
+    as well, where the split heuristic's uneven tasks weigh less), one split per
+    resident warp."""
     import synth
     from paper_2306_12141_b200 import recoil as R
-    N = 1 << 25
+    N = 1 << log2n
     sym, mid, h = synth.latent_workload(N, synth.seed_for(6))
     f = np.concatenate([R.recoil_quantize(x, 16) for x in h["hist"]])
     models = {"base": h["base"], "len": h["len"], "f": f}
@@ -752,6 +754,7 @@ def main():
                                     "recoil_over_partitioned": round(float(np.median(r20) / np.median(p20g)), 4)}
         if not args.no_adaptive:
             extra["adaptive_latent"] = adaptive_extra(args, local, stream, timed_decode, peak_hbm())
+            extra["adaptive_latent_2p27"] = adaptive_extra(args, local, stream, timed_decode, peak_hbm(), 27)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the oracle as it stands, one host core, a bounded sample: evenly spaced tasks of this container
