@@ -269,6 +269,7 @@ struct Warp {
   // or above it (see refill).
   uint32_t cursor2;
   int cchunk;        // (cursor2 - 2) >> 9 at the last window check
+  uint32_t lo2;      // (cchunk << 9) + 2: the cursor drops below it when it enters chunk cchunk - 1
 
   // a7: warp-cooperative prefetch of word chunk c (256 words = 32 lanes x 16 B)
   __device__ __forceinline__ void issue_chunk(int c) {
@@ -281,13 +282,14 @@ struct Warp {
   // 4-chunk ring).  16 groups consume at most 512 words (two chunks), so one
   // check covers a whole output block.
   __device__ __forceinline__ void window_check() {
-    const int c = (int)((cursor2 - 2u) >> 9);
-    if (c != cchunk) {
+    if (cursor2 < lo2) {  // (cursor2 - 2) >> 9 < cchunk: the cursor only moves down
+      const int c = (int)((cursor2 - 2u) >> 9);
       __syncwarp();  // all lanes' reads of the slot being refilled (chunk c+1's) are done
       do {
         --cchunk;
         issue_chunk(cchunk - 3);
       } while (cchunk > c);
+      lo2 = ((uint32_t)cchunk << 9) + 2u;
       cp_wait<1>();
       __syncwarp();
     }
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
     return;
   }
   w.cchunk = 0;
+  w.lo2 = 2u;
   const uint32_t rec32 = smem_addr(&sm_rec[2 * warp]);
   const uint32_t *lut = sm_lut;
   const uint8_t *sym = sym_dyn;
@@ -600,6 +603,7 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   auto issue_window = [&](int32_t cursor0) {
     w.cursor2 = 2u * (uint32_t)cursor0 + 2u;
     w.cchunk = cursor0 >> 8;
+    w.lo2 = ((uint32_t)w.cchunk << 9) + 2u;
     w.issue_chunk(w.cchunk);
     w.issue_chunk(w.cchunk - 1);
     w.issue_chunk(w.cchunk - 2);
