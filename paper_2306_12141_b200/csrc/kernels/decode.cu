@@ -45,6 +45,9 @@
 
 namespace recoil {
 namespace dev {
+#ifdef RECOIL_CHECK_BOUNDS
+__device__ unsigned long long g_oob;  // output stores outside the plan's buffer (debug builds)
+#endif
 
 // Warps per block.  The SM's warp schedulers favour older CTAs: with one task
 // per warp, the warps of the last-resident CTA get issue slots only when the
@@ -308,6 +311,25 @@ struct Warp {
     return need ? x * 65536u + w : x;
   }
   // Eq. 2 with the LUT; stages the symbol byte of group slot k (= g mod 16)
+#ifdef RECOIL_CHECK_BOUNDS
+  // debug builds (tools/build_variant.sh -DRECOIL_CHECK_BOUNDS; compute-sanitizer is not
+  // available on the GPU pool): every output store is checked against the plan's
+  // output buffer [chk_lo, chk_hi); a store outside it is counted (g_oob) and dropped
+  uint8_t *chk_lo, *chk_hi;
+  __device__ __forceinline__ bool in_out(const uint8_t *a, uint32_t n) const { return a >= chk_lo && a + n <= chk_hi; }
+#else
+  __device__ __forceinline__ bool in_out(const uint8_t *, uint32_t) const { return true; }
+#endif
+  template <int S>
+  __device__ __forceinline__ void st_out(uint8_t *a, uint32_t v) {
+    if (!in_out(a, S)) return oob();
+    if (S == 1) stg_u8(a, v); else stg_u16(a, v);
+  }
+  __device__ __forceinline__ void st_out16(uint8_t *a, int4 v) {
+    if (!in_out(a, 16)) return oob();
+    stg_v4(a, v);
+  }
+  __device__ __forceinline__ void oob() const;
   uint8_t *outp = nullptr;  // whole blocks: this lane's symbol (S bytes) of group 0 of the output block
   template <int NB, bool DIRECT = false>
   __device__ __forceinline__ uint32_t decode(const uint32_t *lut, const uint8_t *sym, uint32_t x, uint32_t k) {
@@ -336,7 +358,7 @@ struct Warp {
       }
       const uint32_t e = lds_u32(ent32 + 4 * lo);
       if constexpr (DIRECT)  // whole blocks: straight to HBM (64 B = two full sectors per warp)
-        stg_u16(outp + k * 64, lo + lds_u32(delta32 + 4 * km));
+        st_out<2>(outp + k * 64, lo + lds_u32(delta32 + 4 * km));
       else
         sts_u16(stage32 + k * 64, lo + lds_u32(delta32 + 4 * km));
       return ((e >> 16) + 1) * (x >> nb) + slot - (e & 0xFFFFu);  // f (x >> n) + slot - F
@@ -352,7 +374,7 @@ struct Warp {
         e = lds_u32(lut32 + ((x & ((1u << NB) - 1)) << 2));
       }
       if constexpr (DIRECT)
-        stg_u8(outp + k * 32, e);  // whole blocks: straight to HBM (one 32-B sector per warp)
+        st_out<1>(outp + k * 32, e);  // whole blocks: straight to HBM (one 32-B sector per warp)
       else
         sts_u8(stage32 + k * 32, e);
       // f (x >> n) + bias as f ((x >> n) - 2^12) + (e >> 8), since e >> 8 = bias + 2^12 f
@@ -376,8 +398,8 @@ struct Warp {
     __syncwarp();
     if (c >= woff && c + 16 * S <= wend) {
       const uint32_t a = stage32 + (16 * S - S) * lane;  // staging base + 16 S lane
-      stg_v4(dst + 16 * S * lane, lds_v4(a));
-      if (S == 2) stg_v4(dst + 32 * lane + 16, lds_v4(a + 16));
+      st_out16(dst + 16 * S * lane, lds_v4(a));
+      if (S == 2) st_out16(dst + 32 * lane + 16, lds_v4(a + 16));
     }
     __syncwarp();  // the staging block is rewritten by the next group steps
   }
@@ -386,8 +408,8 @@ struct Warp {
   __device__ __forceinline__ void flush_whole(uint8_t *dst) {
     __syncwarp();
     const uint32_t a = stage32 + (16 * S - S) * lane;
-    stg_v4(dst, lds_v4(a));
-    if (S == 2) stg_v4(dst + 16, lds_v4(a + 16));
+    st_out16(dst, lds_v4(a));
+    if (S == 2) st_out16(dst + 16, lds_v4(a + 16));
     __syncwarp();
   }
   template <int S>
@@ -395,6 +417,12 @@ struct Warp {
     flush_at<S>(dst, rel + 16 * S * lane, woff, wend);
   }
 };
+
+__device__ __forceinline__ void Warp::oob() const {
+#ifdef RECOIL_CHECK_BOUNDS
+  atomicAdd(&g_oob, 1ull);
+#endif
+}
 
 // One group step.  SYNC: Synchronization Phase logic -- lane j is
 // initialised with its anchor state in its anchor group, before its read;
@@ -539,6 +567,13 @@ __global__ void __launch_bounds__(threads_per_block<NB>(), min_blocks<NB>()) rec
   w.stage32 = smem_addr(smem_dyn + L::kStage + warp * (int)kBlockBytes * S + S * lane);
   w.ge = lanemask_ge();
   w.lut32 = smem_addr(sm_lut);
+#ifdef RECOIL_CHECK_BOUNDS
+  w.chk_lo = p.out;
+  w.chk_hi = p.out + (p.out_lim - p.out_base) * S;
+#ifdef RECOIL_CHECK_SELFTEST
+  w.chk_hi -= 512;  // positive control of the check: the last block's stores count as out of bounds
+#endif
+#endif
   if constexpr (NB >= 1 && NB <= kCopyMaxBits) w.lut32 += 4 * (lane / (32 / kLutCopies));  // this lane's copy
   if constexpr (NB <= 0) {
     w.mid32 = w.lut32 + 512 * warp + lane;
@@ -1210,6 +1245,17 @@ extern "C" int recoil_decode_occupancy(int device, uint32_t nbits, int *warps_pe
   return RECOIL_OK;
 }
 
+#ifdef RECOIL_CHECK_BOUNDS
+// debug builds: out-of-buffer output stores counted since the last reset
+extern "C" int recoil_debug_oob(unsigned long long *count, int reset) {
+  if (cudaMemcpyFromSymbol(count, recoil::dev::g_oob, sizeof(*count)) != cudaSuccess) return RECOIL_E_CUDA;
+  if (reset) {
+    const unsigned long long z = 0;
+    if (cudaMemcpyToSymbol(recoil::dev::g_oob, &z, sizeof(z)) != cudaSuccess) return RECOIL_E_CUDA;
+  }
+  return RECOIL_OK;
+}
+#endif
 #ifdef RECOIL_TIMELINE
 extern "C" int recoil_timeline_read(unsigned long long *host, uint32_t n_tasks) {
   const uint32_t n = n_tasks < recoil::dev::kTimelineMax ? n_tasks : recoil::dev::kTimelineMax;
